@@ -1,0 +1,397 @@
+#!/usr/bin/env python
+"""bench.py — PPF input GB/s, x real-time (6.5 GB/s) and HBM-roofline fraction
+on 1..8 B200 (BASELINE.json metric), one process per GPU.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config ska|cfg1|...]
+                  [--mode fast|exact|unfused] [--impl ours|reference]
+
+A step = one pass of the fused FIR+FFT hot path (ppfg_fir_fft) over one
+batch: the whole SKA-LFAA second (C=1024, T=8, 793,457 spectra = 6.5e9 B)
+per GPU. With N GPUs every rank takes the next contiguous 6.5 GB segment of
+one stream (+ its (T-1)-spectrum halo, generated in place: no communication),
+so per-GPU work is fixed ("weak"); value = all ranks' input bytes / the max
+over ranks of the device-timed region.
+
+`value`   device-resident (inputs already in HBM), CUDA events on the kernel's
+          stream, barrier + synchronize around the K timed steps.
+`e2e`     the same metric through the public C-ABI call with HOST buffers
+          (pinned): every step copies the input H2D and the spectra D2H inside
+          ppfg_fir_fft's chunked double-buffered pipeline.
+`roofline` the dominant (only) kernel: algorithmic bytes 8*C*(S_in+S_out) per
+          launch / mean launch time vs the measured HBM copy peak.
+`cpu_baseline` the reference's own CPU compute pass (oracle/_ref: carry_history
+          -> ppf_fir_optimized -> channelize_block, bench.hpp:129-150) on all
+          host cores, on a bounded 1 GiB sample, rank 0 at N=1 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PPF input GB/s & ×real-time (6.5 GB/s) vs HBM roofline at 1/2/4/8 B200"
+SKA_RATE = 6.5e9                      # bytes/s, pipeline.hpp:17
+FALLBACK_HBM_GBS = 6650.0             # /opt/skills/guides/B200_PROFILING.md fallback
+
+CONFIGS = {
+    # name: (C, T, S_in per GPU, description)
+    "ska": (1024, 8, 793_457, "SKA-LFAA single channel: C=1024, T=8, 793,457 spectra "
+                              "(6.5e9 B, 1 s) complex fp32 per GPU"),
+    "cfg1": (512, 8, 1 << 17, "PPF C=512, T=8, 2^17 spectra complex fp32"),
+    "long16": (1024, 16, 7_812_500, "long stream C=1024, T=16, 64e9 B (sharded)"),
+}
+
+
+def max_over_ranks(x: float) -> float:
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(x)
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" \
+        else torch.device("cpu")
+    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x: float) -> float:
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(x)
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" \
+        else torch.device("cpu")
+    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([v.strip() for v in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            if len(r) >= 9:
+                for k, v in zip(names, r[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(k)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_reference_sample(C, T, coeffs, sample_spectra, reps, workers):
+    """Time the reference's own CPU compute pass (bench.hpp:129-150) on a bounded
+    sample of the same workload. Returns (GB/s of input, kind, cores, seconds)."""
+    import oracle
+    from paper_1411_3656_b200 import ppf
+    x = ppf.synth(C, sample_spectra * C, seed=1)
+    ref = oracle.reference()
+    if ref is not None:
+        secs, emitted = ref.compute_pass(x, C, T, coeffs, block_spectra=4096, workers=workers,
+                                         reps=reps + 1)
+        secs = secs[1:]  # first rep is the warm-up (bench.hpp:152-153)
+        kind, cores = "reference", workers
+    else:
+        port = oracle.port()
+        secs = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            port.fir_fft(x, C, T, coeffs)
+            secs.append(time.perf_counter() - t0)
+        kind, cores = "port", 1
+    t = float(np.median(secs))
+    return sample_spectra * C * 8 / t / 1e9, kind, cores, secs
+
+
+def run_reference_arm(args, rank, world):
+    """--impl reference: the reference's CPU implementation of the path on this
+    box's host cores (oracle/_ref), rank 0 only."""
+    if rank != 0:
+        return
+    C, T, S_in, desc = CONFIGS[args.config]
+    from paper_1411_3656_b200 import ppf
+    coeffs = ppf.generate_prototype(C, T).values
+    workers = os.cpu_count() or 1
+    sample = max(T, (args.cpu_sample_mib << 20) // (C * 8))
+    import oracle
+    ref = oracle.reference()
+    x = ppf.synth(C, sample * C, seed=1)
+    step_times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        if ref is not None:
+            ref.compute_pass(x, C, T, coeffs, block_spectra=4096, workers=workers, reps=1)
+        else:
+            oracle.port().fir_fft(x, C, T, coeffs)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            step_times.append(dt)
+    kind = "reference" if ref is not None else "port"
+    cores = workers if ref is not None else 1
+    t = float(np.mean(step_times))
+    gbs = sample * C * 8 / t / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64-acc FIR + f32 FFT (CPU)", "data": "synthetic",
+        "x_realtime": gbs * 1e9 / SKA_RATE,
+        "config": {"workload": desc, "n_channels": C, "n_taps": T,
+                   "sample_spectra": sample, "sample_bytes": sample * C * 8},
+        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": cores, "kind": kind,
+                         "sample": f"{sample} spectra ({sample * C * 8 / 2**20:.0f} MiB) of the "
+                                   f"{args.config} workload per step, compute pass with "
+                                   f"block_spectra=4096, workers={cores}"},
+        "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="ska", choices=sorted(CONFIGS))
+    ap.add_argument("--mode", default="fast", choices=["fast", "exact", "unfused"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-mib", type=int, default=1024)
+    ap.add_argument("--spectra", type=int, default=0, help="override S_in per GPU")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    dev = torch.device("cuda", local_rank)
+    from paper_1411_3656_b200 import ppf
+
+    C, T, S_per, desc = CONFIGS[args.config]
+    if args.spectra:
+        S_per = args.spectra
+    if args.config == "long16":
+        # the 64e9-byte stream is SHARDED across ranks (strong scaling)
+        S_total = S_per
+        ib, ic, ob, oc = ppf.shard_range(S_total, T, rank, world)
+        scaling = "strong"
+    else:
+        # every rank its own contiguous S_per-spectrum segment of one stream
+        S_total = S_per * world + T - 1
+        ib, ic, ob, oc = ppf.shard_range(S_total, T, rank, world)
+        scaling = "weak"
+    flags = {"fast": ppf.FAST, "exact": ppf.EXACT, "unfused": ppf.UNFUSED}[args.mode]
+    coeffs = ppf.generate_prototype(C, T)
+    plan = ppf.Plan(C, T, coeffs, flags=flags, device=local_rank)
+    stream = torch.cuda.current_stream(dev)
+
+    x = torch.empty((ic, C), dtype=torch.complex64, device=dev)
+    y = torch.empty((oc, C), dtype=torch.complex64, device=dev)
+    ppf.synth(C, ic * C, seed=1, first_sample=ib * C, out=x)   # the shard + its halo, in place
+    torch.cuda.synchronize()
+
+    bytes_in = ic * C * 8          # per rank, halo included (it is read)
+    bytes_out = oc * C * 8
+    alg_bytes = bytes_in + bytes_out
+
+    def step():
+        plan.fir_fft(x, out=y)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    time.sleep(0.3)
+    launches0 = ppf.kernel_launches()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    per_launch = []
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        step()
+        b.record(stream)
+        per_launch.append((a, b))
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = ppf.kernel_launches() - launches0
+    clocks = sampler.stop()
+    t_total = ev0.elapsed_time(ev1) / 1e3
+    t_launch = float(np.mean([a.elapsed_time(b) for a, b in per_launch])) / 1e3
+    t_max = max_over_ranks(t_total)
+    in_all = sum_over_ranks(bytes_in)
+    value = in_all * args.steps / t_max / 1e9
+
+    peak, peak_src = measured_peak()
+    achieved = alg_bytes / t_launch / 1e9
+
+    # ---- correctness spot check of the timed output (sampled rows vs oracle) ----
+    spot = None
+    if rank == 0:
+        import oracle
+        rows = [0, oc // 2, oc - 1]
+        errs = []
+        for r in rows:
+            lo = max(r - 2, 0)
+            hi = min(r + 3, oc)
+            xin = x[lo:hi + T - 1].cpu().numpy()
+            want = oracle.port().fir_fft(xin, C, T, coeffs.values).view(np.complex64)
+            got = y[lo:hi].cpu().numpy().reshape(-1)
+            d = np.abs(got.astype(np.complex128) - want.astype(np.complex128)).max()
+            errs.append(d / np.sqrt(np.mean(np.abs(want.astype(np.complex128)) ** 2)))
+        spot = float(max(errs))
+
+    # ---- end to end through the public C-ABI with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        hx = torch.empty((ic, C), dtype=torch.complex64, pin_memory=True)
+        hy = torch.empty((oc, C), dtype=torch.complex64, pin_memory=True)
+        hx.copy_(x)
+        torch.cuda.synchronize()
+        plan.fir_fft(hx, out=hy)  # warm-up (allocates the pipeline buffers)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            plan.fir_fft(hx, out=hy)
+            _ = float(hy[-1, 0].real)   # host read of the step's result
+        te = time.perf_counter() - t0
+        te_max = max_over_ranks(te)
+        row_b = C * 8
+        chunk = max(1, min(oc, (64 << 20) // row_b))
+        n_chunks = -(-oc // chunk)
+        h2d = (oc + n_chunks * (T - 1)) * row_b
+        e2e = {"value": in_all * args.e2e_steps / te_max / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(oc * row_b),
+               "steps": args.e2e_steps, "x_realtime": in_all * args.e2e_steps / te_max / SKA_RATE,
+               "path": "ppfg_fir_fft(mem=HOST), pinned buffers, 64 MiB double-buffered chunks"}
+        del hx, hy
+
+    # ---- CPU baseline: the reference on this host, N=1 rank 0 only ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        workers = os.cpu_count() or 1
+        sample = max(T, (args.cpu_sample_mib << 20) // (C * 8))
+        gbs, kind, cores, secs = cpu_reference_sample(C, T, coeffs.values, sample, 2, workers)
+        cpu = {"value": gbs, "unit": "GB/s", "cores": cores, "kind": kind,
+               "sample": f"{sample} spectra ({sample * C * 8 / 2**20:.0f} MiB) of the same "
+                         f"workload, reference compute pass (bench.hpp:129-150), "
+                         f"block_spectra=4096, median of {len(secs)}",
+               "x_realtime": gbs * 1e9 / SKA_RATE}
+
+    if rank == 0:
+        kind = plan.kind
+        line = {
+            "metric": METRIC,
+            "value": value,
+            "unit": "GB/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": t_max / args.steps * 1e3,
+            "higher_is_better": True,
+            "scaling": scaling,
+            "vs_baseline": None,
+            "dtype": {"fast": "f32", "exact": "f64-acc FIR + f32 FFT",
+                      "unfused": "f64-acc FIR + f32 FFT"}[args.mode],
+            "data": "synthetic (counter-based tone+noise, generated on device per shard)",
+            "x_realtime": value * 1e9 / SKA_RATE,
+            "config": {"workload": desc, "n_channels": C, "n_taps": T,
+                       "n_spectra_in_per_gpu": ic, "bytes_in_per_gpu": bytes_in,
+                       "mode": args.mode, "kernel": ["unfused", "fused-fp32", "fused-fp64"][kind],
+                       "l2": "inputs >> 126 MB L2 (no flush needed)", "parallelism": f"shard{world}"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                         "bytes_per_launch": alg_bytes,
+                         "launch_ms": t_launch * 1e3},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clocks,
+            "gpu_launches": int(launches),
+            "spot_check_max_err_over_rms": spot,
+        }
+        print(json.dumps(line), flush=True)
+    plan.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

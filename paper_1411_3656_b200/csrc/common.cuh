@@ -1,0 +1,99 @@
+// common.cuh — shared device helpers for the sm_100a PPF kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define PPFG_DEV __device__ __forceinline__
+#define PPFG_HD __host__ __device__ __forceinline__
+
+namespace ppfg {
+
+// ---- compile-time bit helpers -------------------------------------------------
+PPFG_HD constexpr unsigned crev(unsigned x, int nbits) {
+    unsigned r = 0;
+    for (int i = 0; i < nbits; ++i)
+        r |= ((x >> i) & 1u) << (nbits - 1 - i);
+    return r;
+}
+
+// runtime reverse of the low nbits (nbits >= 1)
+PPFG_DEV unsigned crev_rt(unsigned x, int nbits) { return __brev(x) >> (32 - nbits); }
+
+// Shared-memory swizzle for float2 rows: base-16 digit sum. Additive over
+// disjoint bit sets (so sw(fixed | k<<LO) = sw(fixed) + sw(k<<LO), giving
+// immediate-offset LDS/STS), and conflict-free whenever the 16 lanes of a
+// half-warp vary any 4 consecutive label bits (their contributions mod 16 are
+// 4 distinct powers of two).
+PPFG_HD constexpr unsigned sw(unsigned n) { return n + (n >> 4) + (n >> 8) + (n >> 12); }
+PPFG_HD constexpr unsigned sw_row_stride(unsigned N) { return ((sw(N - 1) + 1) + 1) & ~1u; }
+
+// ---- the reference's radix-2 butterfly (dft.hpp:122-131), exact -------------
+// tr = fma(br, wr, -(bi*wi)); ti = fma(br, wi, bi*wr); hi = lo - t; lo += t.
+// The _rn intrinsics forbid contraction so every operation rounds exactly as
+// the reference's explicit std::fma / float ops do.
+PPFG_DEV void bfly(float2& lo, float2& hi, const float2 w) {
+    const float br = hi.x, bi = hi.y;
+    const float tr = __fmaf_rn(br, w.x, -__fmul_rn(bi, w.y));
+    const float ti = __fmaf_rn(br, w.y, __fmul_rn(bi, w.x));
+    hi.x = __fsub_rn(lo.x, tr);
+    hi.y = __fsub_rn(lo.y, ti);
+    lo.x = __fadd_rn(lo.x, tr);
+    lo.y = __fadd_rn(lo.y, ti);
+}
+
+// ---- mbarrier / bulk-copy (TMA 1-D) PTX wrappers --------------------------------
+PPFG_DEV uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+PPFG_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+}
+
+PPFG_DEV void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+PPFG_DEV void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+PPFG_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+PPFG_DEV bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
+PPFG_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+    while (!mbar_try_wait(bar, parity)) {
+    }
+}
+
+// global -> shared bulk copy completing on an mbarrier (SASS: UBLKCP).
+// bytes % 16 == 0, both addresses 16-byte aligned.
+PPFG_DEV void bulk_g2s(void* smem_dst, const void* gmem_src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(smem_dst)),
+        "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// streaming (evict-first) 8-byte global store
+PPFG_DEV void st_cs(float2* p, float2 v) { __stcs(p, v); }
+
+} // namespace ppfg

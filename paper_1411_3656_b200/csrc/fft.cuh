@@ -1,0 +1,187 @@
+// fft.cuh — the reference's radix-2 DIT FFT (dft.hpp:72-148), bit-exact, as a
+// register/shared-memory pass engine for sm_100a.
+//
+// Formulation. The reference bit-reverses a row, then runs stages
+// len = 2, 4, ..., N; stage s (half h = 2^{s-1}) pairs positions p, p + h and
+// uses twiddle tw[h-1+j], j = p mod h (dft.hpp:113-133). Track each element by
+// its LABEL n = rev_L(p) instead (the channel index it started from): stage s
+// pairs labels differing in bit b = L - s, and j = rev_{s-1}(n >> (b+1)). After
+// the last stage label n holds bin rev_L(n). So a thread that holds the 2^W
+// elements whose labels differ only in bits [LO, LO+W) can run those W stages
+// in registers, with exactly the reference's butterflies and twiddles, and
+// element-wise results are bit-identical to FftPlan::transform.
+//
+// A row is processed in passes of <= W label bits from the top bit down.
+// Between passes elements go through shared memory at swizzled slot sw(label).
+// Unit (thread task) mapping per pass:
+//   first pass  : fixed label bits [0, LO) = u  -> lanes read consecutive
+//                 channels of the input row (coalesced 8-byte loads);
+//   middle pass : fixed bits = (low LO bits of u) | (rest of u above the pass);
+//   final pass  : fixed bits [W, L) = rev(u), so element k is bin u + rev_L(k)
+//                 and lanes store consecutive bins (coalesced).
+#pragma once
+
+#include "common.cuh"
+
+namespace ppfg {
+
+template <bool TW_SMEM>
+PPFG_DEV float2 tw_load(const float2* p) {
+    if constexpr (TW_SMEM)
+        return *p;
+    else
+        return __ldg(p);
+}
+
+// Stages for label bits [LO, LO+W), high bit first. v[k] has label fixed|k<<LO.
+template <int L, int LO, int W, bool TW_SMEM>
+PPFG_DEV void fft_stages(float2 (&v)[1 << W], unsigned fixed, const float2* __restrict__ tw) {
+#pragma unroll
+    for (int bb = W - 1; bb >= 0; --bb) {
+        const int b = LO + bb;
+        const int s = L - b;
+        const unsigned half = 1u << (s - 1);
+        const unsigned jf = (s > 1) ? (__brev(fixed >> (b + 1)) >> (33 - s)) : 0u;
+        const float2* twb = tw + (half - 1) + jf;
+#pragma unroll
+        for (int k = 0; k < (1 << W); ++k) {
+            if (k & (1 << bb))
+                continue;
+            const unsigned jk = crev((static_cast<unsigned>(k) << LO) >> (b + 1), s - 1);
+            const float2 w = tw_load<TW_SMEM>(twb + jk);
+            bfly(v[k], v[k | (1 << bb)], w);
+        }
+    }
+}
+
+// ---- pass schedule: NP passes of near-equal width, widest first ------------------
+template <int L, int W>
+struct FftSchedule {
+    static constexpr int NP = L == 0 ? 1 : (L + W - 1) / W;
+    static constexpr int width(int i) { return L / NP + (i < L % NP ? 1 : 0); }
+    static constexpr int done(int i) { return i * (L / NP) + (i < L % NP ? i : L % NP); }
+    static constexpr int lo(int i) { return L - done(i + 1); }
+};
+
+// One pass of the row engine over a tile of rows.
+//   FIRST_GLOBAL: this (top) pass reads natural-order input rows from global.
+//   FINAL       : this (bit-0) pass writes natural-order bins to global.
+// map(r) gives the global row of tile row r, or -1 for a padding row.
+template <int L, int LO, int W, bool FIRST_GLOBAL, bool FINAL, bool TW_SMEM, int NT, class RowMap>
+// gin/gout may alias (in-place channelize): every row is fully read before it is
+// written, with a barrier in between for multi-pass transforms.
+PPFG_DEV void fft_tile_pass(const float2* gin, float2* gout,
+                            float2* __restrict__ tile, unsigned row_stride, int rows,
+                            const RowMap& map, const float2* __restrict__ tw) {
+    constexpr int N = 1 << L;
+    constexpr int E = 1 << W;
+    constexpr int HI = LO + W - 1;
+    constexpr int U = N >> W;
+    static_assert(!FIRST_GLOBAL || HI == L - 1, "a global-source pass must be the top pass");
+    static_assert(!FINAL || LO == 0, "the final pass ends at label bit 0");
+    const int units = rows * U;
+    for (int unit = threadIdx.x; unit < units; unit += NT) {
+        const int r = unit / U;
+        const unsigned u = static_cast<unsigned>(unit % U);
+        unsigned fixed;
+        if constexpr (FINAL)
+            fixed = (L - W > 0) ? (crev_rt(u, L - W) << W) : 0u;
+        else if constexpr (FIRST_GLOBAL)
+            fixed = u;
+        else
+            fixed = (u & ((1u << LO) - 1u)) | ((u >> LO) << (HI + 1));
+        float2 v[E];
+        if constexpr (FIRST_GLOBAL) {
+            const long long grow = map(r);
+            const float2* src = gin + grow * N + fixed;
+#pragma unroll
+            for (int k = 0; k < E; ++k)
+                v[k] = grow >= 0 ? src[static_cast<unsigned>(k) << LO] : make_float2(0.f, 0.f);
+        } else {
+            const float2* src = tile + r * row_stride + sw(fixed);
+#pragma unroll
+            for (int k = 0; k < E; ++k)
+                v[k] = src[sw(static_cast<unsigned>(k) << LO)];
+        }
+        fft_stages<L, LO, W, TW_SMEM>(v, fixed, tw);
+        if constexpr (FINAL) {
+            const long long grow = map(r);
+            if (grow >= 0) {
+                float2* dst = gout + grow * N + u;
+#pragma unroll
+                for (int k = 0; k < E; ++k)
+                    st_cs(dst + crev(static_cast<unsigned>(k), L), v[k]);
+            }
+        } else {
+            float2* dst = tile + r * row_stride + sw(fixed);
+#pragma unroll
+            for (int k = 0; k < E; ++k)
+                dst[sw(static_cast<unsigned>(k) << LO)] = v[k];
+        }
+    }
+}
+
+// The passes covering label bits [0, LREM) of an N = 2^L transform (the top
+// L - LREM bits were already done, e.g. in the fused kernel's FIR threads).
+template <int L, int LREM, int W, bool FIRST_GLOBAL, bool TW_SMEM, int NT, int I = 0>
+struct FftPasses {
+    using S = FftSchedule<LREM, W>;
+    static constexpr int WI = S::width(I);
+    static constexpr int LO = S::lo(I);
+    static constexpr bool FINAL = (I == S::NP - 1);
+    template <class RowMap>
+    PPFG_DEV static void run(const float2* gin, float2* gout, float2* tile, unsigned row_stride,
+                             int rows, const RowMap& map, const float2* tw) {
+        fft_tile_pass<L, LO, WI, FIRST_GLOBAL && I == 0, FINAL, TW_SMEM, NT>(
+            gin, gout, tile, row_stride, rows, map, tw);
+        if constexpr (!FINAL) {
+            __syncthreads();
+            FftPasses<L, LREM, W, FIRST_GLOBAL, TW_SMEM, NT, I + 1>::run(gin, gout, tile,
+                                                                          row_stride, rows, map, tw);
+        }
+    }
+};
+
+struct LinearRows {
+    long long row0, n_rows;
+    PPFG_DEV long long operator()(int r) const {
+        return row0 + r < n_rows ? row0 + r : -1;
+    }
+};
+
+// K2: channelize_block for power-of-two C = 2^L (L >= 1), rows independent.
+// Persistent grid; each CTA transforms RB = max(1, NT*2^W/N) rows per tile.
+template <int L, int W, bool TW_SMEM, int NT>
+__global__ void __launch_bounds__(NT) fft_rows_kernel(const float2* in, float2* out,
+                                                      long long n_rows,
+                                                      const float2* __restrict__ tw_g) {
+    constexpr int N = 1 << L;
+    constexpr int RB = (NT << W) / N > 0 ? (NT << W) / N : 1;
+    extern __shared__ float2 smem[];
+    float2* tw_s = smem;
+    float2* tile = smem + (TW_SMEM ? ((N + 1) & ~1) : 0);
+    if constexpr (TW_SMEM) {
+        for (int i = threadIdx.x; i < N - 1; i += NT)
+            tw_s[i] = tw_g[i];
+        __syncthreads();
+    }
+    const float2* tw = TW_SMEM ? tw_s : tw_g;
+    constexpr unsigned stride = sw_row_stride(N);
+    for (long long row0 = static_cast<long long>(blockIdx.x) * RB; row0 < n_rows;
+         row0 += static_cast<long long>(gridDim.x) * RB) {
+        FftPasses<L, L, W, true, TW_SMEM, NT>::run(in, out, tile, stride, RB,
+                                                   LinearRows{row0, n_rows}, tw);
+        __syncthreads();
+    }
+}
+
+template <int L, int W, bool TW_SMEM, int NT>
+constexpr size_t fft_rows_smem_bytes() {
+    constexpr int N = 1 << L;
+    constexpr int RB = (NT << W) / N > 0 ? (NT << W) / N : 1;
+    constexpr bool multipass = FftSchedule<L, W>::NP > 1;
+    return sizeof(float2) * ((TW_SMEM ? ((N + 1) & ~1) : 0) +
+                             (multipass ? static_cast<size_t>(RB) * sw_row_stride(N) : 0));
+}
+
+} // namespace ppfg

@@ -1,0 +1,1153 @@
+// ppfg.cu — libppfg.so: plans, kernel dispatch, the host-streamed pipeline,
+// device-resident streaming state, multi-GPU sharding and the C-ABI of
+// include/ppfg.h. Kernels live in fir.cuh (K1), fft.cuh (K2), fused.cuh (K3),
+// dft.cuh (K4 dft_naive, K5 synth).
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "ppfg.h"
+
+#include "dft.cuh"
+#include "fft.cuh"
+#include "fir.cuh"
+#include "fused.cuh"
+
+namespace {
+
+using namespace ppfg;
+
+// ------------------------------------------------------------------ errors
+thread_local std::string g_err;
+thread_local uint64_t g_err_offset = 0;
+std::atomic<uint64_t> g_launches{0};
+
+int fail(int status, const std::string& msg) {
+    g_err = msg;
+    return status;
+}
+
+#define PPFG_CUDA(call)                                                                           \
+    do {                                                                                          \
+        cudaError_t e_ = (call);                                                                  \
+        if (e_ != cudaSuccess)                                                                    \
+            return fail(PPFG_CUDA_ERROR, std::string(#call) + ": " + cudaGetErrorString(e_));     \
+    } while (0)
+
+#define PPFG_TRY(expr)                                                                            \
+    do {                                                                                          \
+        int st_ = (expr);                                                                         \
+        if (st_ != PPFG_OK)                                                                       \
+            return st_;                                                                           \
+    } while (0)
+
+int check_launch(const char* what) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess)
+        return fail(PPFG_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+    return PPFG_OK;
+}
+
+bool is_pow2(uint64_t n) { return n != 0 && (n & (n - 1)) == 0; }
+int ilog2(uint64_t n) {
+    int l = 0;
+    while ((uint64_t(1) << l) < n)
+        ++l;
+    return l;
+}
+uint64_t cdiv(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+// RAII device guard
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev)
+            cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev)
+            cudaSetDevice(prev);
+    }
+};
+
+// -------------------------------------------------------- kernel tables
+using KernelFn = const void*;
+
+struct FusedEntry {
+    int L, T;
+    bool exact;
+    KernelFn fn;
+    size_t smem;
+    int nt;
+    int rows_per_batch; // B * G
+};
+
+template <class Cfg>
+FusedEntry fused_entry() {
+    return {Cfg::L, Cfg::T, Cfg::EXACT, reinterpret_cast<KernelFn>(&fused_fir_fft_kernel<Cfg>),
+            Cfg::SMEM, Cfg::NT, Cfg::B * Cfg::G};
+}
+
+// Which (C, T) get a fused kernel. Register budget per SM ~ C * (3T fp32 |
+// 6T fp64) for the FIR windows + taps, plus the FFT pass registers.
+const std::vector<FusedEntry>& fused_table() {
+    static const std::vector<FusedEntry> t = {
+        fused_entry<FusedCfg<9, 8, 2, false>>(),
+        fused_entry<FusedCfg<10, 8, 2, false>>(),
+        fused_entry<FusedCfg<9, 8, 1, true>>(),
+    };
+    return t;
+}
+
+struct FftEntry {
+    KernelFn fn;
+    size_t smem;
+    int nt;
+    int rows_per_tile;
+};
+
+constexpr int kFftW = 5;
+constexpr int kFftNT = 256;
+constexpr int kFftMaxL = 13;
+
+template <int L>
+FftEntry fft_entry() {
+    constexpr bool tws = L <= 11;
+    constexpr int rb = (kFftNT << kFftW) / (1 << L) > 0 ? (kFftNT << kFftW) / (1 << L) : 1;
+    return {reinterpret_cast<KernelFn>(&fft_rows_kernel<L, kFftW, tws, kFftNT>),
+            fft_rows_smem_bytes<L, kFftW, tws, kFftNT>(), kFftNT, rb};
+}
+
+const FftEntry* fft_table(int L) {
+    static const FftEntry t[kFftMaxL + 1] = {
+        {nullptr, 0, 0, 0},  fft_entry<1>(),  fft_entry<2>(),  fft_entry<3>(),  fft_entry<4>(),
+        fft_entry<5>(),      fft_entry<6>(),  fft_entry<7>(),  fft_entry<8>(),  fft_entry<9>(),
+        fft_entry<10>(),     fft_entry<11>(), fft_entry<12>(), fft_entry<13>(),
+    };
+    if (L < 1 || L > kFftMaxL)
+        return nullptr;
+    return &t[L];
+}
+
+KernelFn fir_table(int T) {
+    switch (T) {
+#define PPFG_FIR_CASE(t)                                                                          \
+    case t:                                                                                       \
+        return reinterpret_cast<KernelFn>(&fir_exact_kernel<t>);
+        PPFG_FIR_CASE(1) PPFG_FIR_CASE(2) PPFG_FIR_CASE(3) PPFG_FIR_CASE(4) PPFG_FIR_CASE(5)
+        PPFG_FIR_CASE(6) PPFG_FIR_CASE(7) PPFG_FIR_CASE(8) PPFG_FIR_CASE(9) PPFG_FIR_CASE(10)
+        PPFG_FIR_CASE(11) PPFG_FIR_CASE(12) PPFG_FIR_CASE(13) PPFG_FIR_CASE(14)
+        PPFG_FIR_CASE(15) PPFG_FIR_CASE(16)
+#undef PPFG_FIR_CASE
+    default:
+        return nullptr;
+    }
+}
+
+// one-time per (device, function) opt-in to large dynamic shared memory
+int ensure_smem_attr(KernelFn fn, size_t smem, int device) {
+    static std::mutex mu;
+    static std::map<std::pair<int, KernelFn>, size_t> done;
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_pair(device, fn);
+    auto it = done.find(key);
+    if (it != done.end() && it->second >= smem)
+        return PPFG_OK;
+    if (smem > 48 * 1024)
+        PPFG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem)));
+    done[key] = smem;
+    return PPFG_OK;
+}
+
+} // namespace
+
+// ================================================================== plans
+struct ppfg_plan_s {
+    int device = 0;
+    uint64_t C = 0, T = 0;
+    uint32_t flags = 0;
+    int L = -1; // log2 C when C is a power of two
+    int num_sms = 148;
+    float* d_taps = nullptr;     // [T][C] f32
+    float2* d_tw = nullptr;      // FftPlan twiddles, C-1 entries
+    double2* d_roots = nullptr;  // dft_naive roots, C entries (non-pow2)
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    const FusedEntry* fused = nullptr;
+    // host-mode pipeline buffers (grow-only)
+    void* d_in[2] = {nullptr, nullptr};
+    void* d_out[2] = {nullptr, nullptr};
+    size_t d_in_bytes = 0, d_out_bytes = 0;
+    void* h_in[2] = {nullptr, nullptr}; // pinned staging for pageable callers
+    void* h_out[2] = {nullptr, nullptr};
+    size_t h_in_bytes = 0, h_out_bytes = 0;
+    cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+    cudaEvent_t ev_h2d[2] = {}, ev_comp[2] = {}, ev_d2h[2] = {};
+};
+
+namespace {
+
+// FftPlan twiddles exactly as dft.hpp:88-98: double angle -> cos/sin -> f32.
+std::vector<float2> host_twiddles(uint64_t n) {
+    std::vector<float2> tw(n > 1 ? n - 1 : 1);
+    for (uint64_t len = 2; len <= n; len <<= 1) {
+        const uint64_t half = len / 2;
+        for (uint64_t j = 0; j < half; ++j) {
+            const double angle = -2.0 * M_PI * static_cast<double>(j) / static_cast<double>(len);
+            tw[half - 1 + j] = make_float2(static_cast<float>(std::cos(angle)),
+                                           static_cast<float>(std::sin(angle)));
+        }
+    }
+    return tw;
+}
+
+// dft_naive roots (dft.hpp:47-51)
+std::vector<double2> host_roots(uint64_t n) {
+    std::vector<double2> r(n);
+    for (uint64_t j = 0; j < n; ++j) {
+        const double angle = -2.0 * M_PI * static_cast<double>(j) / static_cast<double>(n);
+        r[j] = make_double2(std::cos(angle), std::sin(angle));
+    }
+    return r;
+}
+
+int stream_of(ppfg_plan p, void* s, cudaStream_t* out) {
+    *out = s ? static_cast<cudaStream_t>(s) : p->stream;
+    return PPFG_OK;
+}
+
+// ---------------------------------------------------------- launchers (device)
+int launch_fir(ppfg_plan p, const float2* din, uint64_t S_in, float2* dout, cudaStream_t st,
+               bool reference_order) {
+    const uint64_t T = p->T, C = p->C;
+    const uint64_t S_out = S_in - T + 1;
+    // segment length: >= 4T outputs so the (T-1) halo stays small; enough
+    // (channel, segment) work items to fill 148 SMs several times over.
+    const uint64_t target_threads = static_cast<uint64_t>(p->num_sms) * 2048 * 2;
+    uint64_t seg = cdiv(S_out * C, target_threads);
+    seg = std::max<uint64_t>(seg, std::min<uint64_t>(4 * T, S_out));
+    seg = std::max<uint64_t>(seg, 1);
+    const uint64_t n_seg = cdiv(S_out, seg);
+    const uint64_t n_work = n_seg * C;
+    const unsigned blocks = static_cast<unsigned>(cdiv(n_work, 256));
+    const double init = reference_order ? 0.0 : -0.0;
+    KernelFn fn = fir_table(static_cast<int>(T));
+    long long S_out_ll = static_cast<long long>(S_out), n_work_ll = static_cast<long long>(n_work);
+    unsigned Cu = static_cast<unsigned>(C);
+    int seg_i = static_cast<int>(seg);
+    if (fn) {
+        void* args[] = {&din, &dout, &Cu, &S_out_ll, &p->d_taps, &seg_i, &n_work_ll,
+                        const_cast<double*>(&init)};
+        PPFG_CUDA(cudaLaunchKernel(fn, dim3(blocks), dim3(256), args, 0, st));
+    } else {
+        fir_exact_generic_kernel<<<blocks, 256, 0, st>>>(din, dout, Cu, static_cast<unsigned>(T),
+                                                          S_out_ll, p->d_taps, seg_i, n_work_ll,
+                                                          init);
+    }
+    return check_launch("fir kernel");
+}
+
+// bit-exact radix-2 for any power-of-two size via global memory (large N)
+__global__ void fft_bitrev_kernel(const float2* in, float2* out, int L, long long n_rows) {
+    const long long g = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const long long N = 1LL << L;
+    if (g >= n_rows * N)
+        return;
+    const long long row = g >> L;
+    const unsigned p = static_cast<unsigned>(g & (N - 1));
+    out[g] = in[row * N + (__brev(p) >> (32 - L))];
+}
+
+__global__ void fft_stage_kernel(float2* data, const float2* __restrict__ tw, int L, int s,
+                                 long long n_rows) {
+    const long long g = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const long long half = 1LL << (s - 1);
+    const long long pairs = 1LL << (L - 1);
+    if (g >= n_rows * pairs)
+        return;
+    const long long row = g >> (L - 1);
+    const long long q = g & (pairs - 1);
+    const long long j = q & (half - 1);
+    const long long base = (q >> (s - 1)) << s;
+    float2* r = data + (row << L);
+    float2 lo = r[base + j], hi = r[base + j + half];
+    bfly(lo, hi, tw[half - 1 + j]);
+    r[base + j] = lo;
+    r[base + j + half] = hi;
+}
+
+int launch_channelize(ppfg_plan p, const float2* din, uint64_t rows, float2* dout,
+                      bool fft_fallback, cudaStream_t st) {
+    if (rows == 0)
+        return PPFG_OK;
+    const uint64_t C = p->C;
+    if (C == 1) { // a 1-point DFT is the identity (both FftPlan(1) and dft_naive)
+        if (din != dout)
+            PPFG_CUDA(cudaMemcpyAsync(dout, din, rows * sizeof(float2), cudaMemcpyDeviceToDevice,
+                                      st));
+        return PPFG_OK;
+    }
+    if (!is_pow2(C)) {
+        if (!fft_fallback)
+            return fail(PPFG_UNSUPPORTED_SIZE,
+                        "channelize_block: non-power-of-two channel count with fallback disabled");
+        const float2* src = din;
+        if (din == dout) { // dft_naive reads the whole row for every bin: not in place
+            void* tmp = nullptr;
+            PPFG_CUDA(cudaMallocAsync(&tmp, rows * C * sizeof(float2), st));
+            PPFG_CUDA(cudaMemcpyAsync(tmp, din, rows * C * sizeof(float2),
+                                      cudaMemcpyDeviceToDevice, st));
+            src = static_cast<const float2*>(tmp);
+        }
+        const uint64_t n = rows * C;
+        dft_naive_kernel<<<static_cast<unsigned>(cdiv(n, 256)), 256, 0, st>>>(
+            src, dout, static_cast<unsigned>(C), static_cast<long long>(rows), p->d_roots);
+        int rc = check_launch("dft_naive kernel");
+        if (src != din)
+            cudaFreeAsync(const_cast<float2*>(src), st);
+        return rc;
+    }
+    const int L = p->L;
+    if (const FftEntry* e = fft_table(L)) {
+        PPFG_TRY(ensure_smem_attr(e->fn, e->smem, p->device));
+        const uint64_t tiles = cdiv(rows, static_cast<uint64_t>(e->rows_per_tile));
+        int per_sm = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, e->fn, e->nt, e->smem);
+        per_sm = std::max(per_sm, 1);
+        const uint64_t grid = std::min<uint64_t>(tiles, static_cast<uint64_t>(p->num_sms) * per_sm);
+        long long rows_ll = static_cast<long long>(rows);
+        void* args[] = {&din, &dout, &rows_ll, &p->d_tw};
+        PPFG_CUDA(cudaLaunchKernel(e->fn, dim3(static_cast<unsigned>(grid)), dim3(e->nt), args,
+                                   e->smem, st));
+        return check_launch("fft kernel");
+    }
+    // L > kFftMaxL: bit reversal then one launch per stage, in global memory
+    float2* buf = dout;
+    void* tmp = nullptr;
+    if (din == dout) {
+        PPFG_CUDA(cudaMallocAsync(&tmp, rows * C * sizeof(float2), st));
+        buf = static_cast<float2*>(tmp);
+    }
+    const long long n = static_cast<long long>(rows * C);
+    fft_bitrev_kernel<<<static_cast<unsigned>(cdiv(n, 256)), 256, 0, st>>>(
+        din, buf, L, static_cast<long long>(rows));
+    PPFG_TRY(check_launch("fft bitrev"));
+    for (int s = 1; s <= L; ++s) {
+        fft_stage_kernel<<<static_cast<unsigned>(cdiv(n / 2, 256)), 256, 0, st>>>(
+            buf, p->d_tw, L, s, static_cast<long long>(rows));
+        PPFG_TRY(check_launch("fft stage"));
+    }
+    if (tmp) {
+        PPFG_CUDA(cudaMemcpyAsync(dout, tmp, rows * C * sizeof(float2), cudaMemcpyDeviceToDevice,
+                                  st));
+        cudaFreeAsync(tmp, st);
+    }
+    return PPFG_OK;
+}
+
+int launch_fused(ppfg_plan p, const float2* din, uint64_t S_in, float2* dout, cudaStream_t st) {
+    const FusedEntry* e = p->fused;
+    PPFG_TRY(ensure_smem_attr(e->fn, e->smem, p->device));
+    const uint64_t S_out = S_in - p->T + 1;
+    const uint64_t grid =
+        std::max<uint64_t>(1, std::min<uint64_t>(p->num_sms, cdiv(S_out, e->rows_per_batch)));
+    long long rows_per_cta = static_cast<long long>(cdiv(S_out, grid));
+    long long S_out_ll = static_cast<long long>(S_out);
+    void* args[] = {&din, &dout, &S_out_ll, &rows_per_cta, &p->d_taps, &p->d_tw};
+    PPFG_CUDA(cudaLaunchKernel(e->fn, dim3(static_cast<unsigned>(grid)), dim3(e->nt), args,
+                               e->smem, st));
+    return check_launch("fused fir+fft kernel");
+}
+
+int launch_fir_fft(ppfg_plan p, const float2* din, uint64_t S_in, float2* dout, cudaStream_t st) {
+    if (p->fused && !(p->flags & PPFG_UNFUSED))
+        return launch_fused(p, din, S_in, dout, st);
+    PPFG_TRY(launch_fir(p, din, S_in, dout, st, false));
+    return launch_channelize(p, dout, S_in - p->T + 1, dout, true, st);
+}
+
+// ------------------------------------------------------ host-mode pipeline
+bool is_pinned(const void* ptr) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged;
+}
+
+int grow_device(void** bufs, size_t* have, size_t need) {
+    if (*have >= need)
+        return PPFG_OK;
+    for (int i = 0; i < 2; ++i) {
+        if (bufs[i])
+            cudaFree(bufs[i]);
+        bufs[i] = nullptr;
+    }
+    for (int i = 0; i < 2; ++i)
+        PPFG_CUDA(cudaMalloc(&bufs[i], need));
+    *have = need;
+    return PPFG_OK;
+}
+
+int grow_pinned(void** bufs, size_t* have, size_t need) {
+    if (*have >= need)
+        return PPFG_OK;
+    for (int i = 0; i < 2; ++i) {
+        if (bufs[i])
+            cudaFreeHost(bufs[i]);
+        bufs[i] = nullptr;
+    }
+    for (int i = 0; i < 2; ++i)
+        PPFG_CUDA(cudaHostAlloc(&bufs[i], need, cudaHostAllocDefault));
+    *have = need;
+    return PPFG_OK;
+}
+
+enum class Op { Fir, FirRef, Channelize, ChannelizeNoFallback, FirFft };
+
+int launch_op(ppfg_plan p, Op op, const float2* din, uint64_t n_in_rows, float2* dout,
+              cudaStream_t st) {
+    switch (op) {
+    case Op::Fir:
+        return launch_fir(p, din, n_in_rows, dout, st, false);
+    case Op::FirRef:
+        return launch_fir(p, din, n_in_rows, dout, st, true);
+    case Op::Channelize:
+        return launch_channelize(p, din, n_in_rows, dout, true, st);
+    case Op::ChannelizeNoFallback:
+        return launch_channelize(p, din, n_in_rows, dout, false, st);
+    case Op::FirFft:
+        return launch_fir_fft(p, din, n_in_rows, dout, st);
+    }
+    return PPFG_CONFIG_ERROR;
+}
+
+constexpr size_t kChunkBytes = size_t(64) << 20;
+
+// Host buffers -> chunked, double-buffered H2D | kernel | D2H on three streams.
+// `halo` input rows overlap between chunks (T-1 for the FIR, 0 for the FFT);
+// output row r depends on input rows r .. r+halo.
+int run_host(ppfg_plan p, Op op, const void* hin, uint64_t n_in_rows, void* hout, uint64_t halo) {
+    const uint64_t row_bytes = p->C * sizeof(float2);
+    const uint64_t n_out_rows = n_in_rows - halo;
+    if (n_out_rows == 0)
+        return PPFG_OK;
+    const uint64_t chunk = std::max<uint64_t>(1, std::min<uint64_t>(n_out_rows,
+                                                                   kChunkBytes / row_bytes));
+    PPFG_TRY(grow_device(p->d_in, &p->d_in_bytes, (chunk + halo) * row_bytes));
+    PPFG_TRY(grow_device(p->d_out, &p->d_out_bytes, chunk * row_bytes));
+    const bool pin_in = is_pinned(hin), pin_out = is_pinned(hout);
+    if (!pin_in)
+        PPFG_TRY(grow_pinned(p->h_in, &p->h_in_bytes, (chunk + halo) * row_bytes));
+    if (!pin_out)
+        PPFG_TRY(grow_pinned(p->h_out, &p->h_out_bytes, chunk * row_bytes));
+    const uint64_t n_chunks = cdiv(n_out_rows, chunk);
+    const char* src = static_cast<const char*>(hin);
+    char* dst = static_cast<char*>(hout);
+    // pending host copy-out of chunk i-2 (pageable outputs)
+    auto drain = [&](uint64_t i) -> int {
+        const int b = static_cast<int>(i & 1);
+        const uint64_t o = i * chunk, n = std::min(chunk, n_out_rows - o);
+        PPFG_CUDA(cudaEventSynchronize(p->ev_d2h[b]));
+        if (!pin_out)
+            std::memcpy(dst + o * row_bytes, p->h_out[b], n * row_bytes);
+        return PPFG_OK;
+    };
+    for (uint64_t i = 0; i < n_chunks; ++i) {
+        const int b = static_cast<int>(i & 1);
+        const uint64_t o = i * chunk, n = std::min(chunk, n_out_rows - o);
+        const uint64_t in_bytes = (n + halo) * row_bytes, out_bytes = n * row_bytes;
+        if (i >= 2)
+            PPFG_TRY(drain(i - 2));
+        // input: d_in[b] is free once chunk i-2's kernel has run
+        if (i >= 2)
+            PPFG_CUDA(cudaStreamWaitEvent(p->s_h2d, p->ev_comp[b], 0));
+        const void* h2d_src = src + o * row_bytes;
+        if (!pin_in) {
+            PPFG_CUDA(cudaEventSynchronize(p->ev_h2d[b])); // staging buffer reusable
+            std::memcpy(p->h_in[b], src + o * row_bytes, in_bytes);
+            h2d_src = p->h_in[b];
+        }
+        PPFG_CUDA(cudaMemcpyAsync(p->d_in[b], h2d_src, in_bytes, cudaMemcpyHostToDevice,
+                                  p->s_h2d));
+        PPFG_CUDA(cudaEventRecord(p->ev_h2d[b], p->s_h2d));
+        // compute: after its input landed and chunk i-2's output left d_out[b]
+        PPFG_CUDA(cudaStreamWaitEvent(p->stream, p->ev_h2d[b], 0));
+        if (i >= 2)
+            PPFG_CUDA(cudaStreamWaitEvent(p->stream, p->ev_d2h[b], 0));
+        PPFG_TRY(launch_op(p, op, static_cast<const float2*>(p->d_in[b]), n + halo,
+                           static_cast<float2*>(p->d_out[b]), p->stream));
+        PPFG_CUDA(cudaEventRecord(p->ev_comp[b], p->stream));
+        // output
+        PPFG_CUDA(cudaStreamWaitEvent(p->s_d2h, p->ev_comp[b], 0));
+        PPFG_CUDA(cudaMemcpyAsync(pin_out ? static_cast<void*>(dst + o * row_bytes) : p->h_out[b],
+                                  p->d_out[b], out_bytes, cudaMemcpyDeviceToHost, p->s_d2h));
+        PPFG_CUDA(cudaEventRecord(p->ev_d2h[b], p->s_d2h));
+    }
+    for (uint64_t i = n_chunks >= 2 ? n_chunks - 2 : 0; i < n_chunks; ++i)
+        PPFG_TRY(drain(i));
+    PPFG_CUDA(cudaStreamSynchronize(p->stream));
+    return PPFG_OK;
+}
+
+int check_plan(ppfg_plan p) {
+    if (!p)
+        return fail(PPFG_CONFIG_ERROR, "ppfg: null plan");
+    return PPFG_OK;
+}
+
+// fir.hpp:56-65 preconditions on an input of n_spectra_in spectra
+int check_fir_input(ppfg_plan p, const void* in, uint64_t n_spectra_in, const void* out) {
+    PPFG_TRY(check_plan(p));
+    if (p->T == 0)
+        return fail(PPFG_CONFIG_ERROR, "fir: malformed coefficient set");
+    if (n_spectra_in == 0)
+        return fail(PPFG_CONFIG_ERROR,
+                    "SampleBlock: sample count must be a positive multiple of n_channels");
+    if (n_spectra_in < p->T)
+        return fail(PPFG_INSUFFICIENT_HISTORY, "fir: need at least n_taps input spectra");
+    if (!in || !out)
+        return fail(PPFG_CONFIG_ERROR, "fir: null buffer");
+    return PPFG_OK;
+}
+
+int run(ppfg_plan p, Op op, const void* in, uint64_t n_in_rows, void* out, int mem, void* s,
+        uint64_t halo) {
+    DeviceGuard dg(p->device);
+    if (mem == PPFG_MEM_DEVICE) {
+        cudaStream_t st;
+        stream_of(p, s, &st);
+        return launch_op(p, op, static_cast<const float2*>(in), n_in_rows, static_cast<float2*>(out),
+                         st);
+    }
+    if (mem != PPFG_MEM_HOST)
+        return fail(PPFG_CONFIG_ERROR, "ppfg: unknown memory kind");
+    return run_host(p, op, in, n_in_rows, out, halo);
+}
+
+// ------------------------------------------------------------ synth tables
+struct ToneCache {
+    std::mutex mu;
+    std::map<std::pair<int, uint64_t>, float2*> dev;
+};
+ToneCache& tone_cache() {
+    static ToneCache c;
+    return c;
+}
+
+std::vector<float2> host_tone(uint64_t C) {
+    const uint64_t M = 10 * C;
+    std::vector<float2> t(M);
+    for (uint64_t k = 0; k < M; ++k) {
+        const double a = 2.0 * M_PI * static_cast<double>(k) / static_cast<double>(M);
+        t[k] = make_float2(static_cast<float>(std::cos(a)), static_cast<float>(std::sin(a)));
+    }
+    return t;
+}
+
+uint64_t tone_f10(uint64_t C) { return (10 * C) / 8 + 3; }
+
+} // namespace
+
+// ================================================================ C-ABI
+extern "C" {
+
+const char* ppfg_version(void) { return "ppfg 0.1 (sm_100a)"; }
+const char* ppfg_last_error(void) { return g_err.c_str(); }
+uint64_t ppfg_last_error_offset(void) { return g_err_offset; }
+uint64_t ppfg_kernel_launches(void) { return g_launches.load(); }
+
+uint64_t ppfg_flops_for_fir(uint64_t n_channels, uint64_t n_taps, uint64_t n_spectra_out) {
+    return n_spectra_out * n_channels * n_taps * 4u; // fir.hpp:49-52
+}
+
+uint64_t ppfg_flops_for_dft(uint64_t n_channels, uint64_t n_spectra) { // dft.hpp:28-35
+    if (is_pow2(n_channels))
+        return n_spectra * 5u * n_channels * static_cast<uint64_t>(ilog2(n_channels));
+    return n_spectra * 8u * n_channels * n_channels;
+}
+
+int ppfg_plan_create(ppfg_plan* plan, uint64_t n_channels, uint64_t n_taps,
+                     const double* coeff_values, uint32_t flags, int device) {
+    if (!plan)
+        return fail(PPFG_CONFIG_ERROR, "ppfg_plan_create: null plan pointer");
+    *plan = nullptr;
+    if (n_channels == 0)
+        return fail(PPFG_CONFIG_ERROR, "SampleBlock: n_channels must be >= 1");
+    if (n_taps > 0 && !coeff_values)
+        return fail(PPFG_CONFIG_ERROR, "fir: malformed coefficient set");
+    if (n_channels > (uint64_t(1) << 24) || n_taps > 4096)
+        return fail(PPFG_CONFIG_ERROR, "ppfg_plan_create: channel or tap count out of range");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(PPFG_NO_DEVICE, "ppfg: no CUDA device");
+    }
+    if (device < 0 || device >= ndev)
+        return fail(PPFG_NO_DEVICE, "ppfg: device index out of range");
+    DeviceGuard dg(device);
+    cudaDeviceProp prop{};
+    PPFG_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10)
+        return fail(PPFG_NO_DEVICE, std::string("ppfg: needs an sm_100 device, found ") + prop.name);
+    auto* p = new ppfg_plan_s();
+    p->device = device;
+    p->C = n_channels;
+    p->T = n_taps;
+    p->flags = flags;
+    p->num_sms = prop.multiProcessorCount;
+    p->L = is_pow2(n_channels) ? ilog2(n_channels) : -1;
+    auto cleanup = [&](int st) {
+        ppfg_plan_destroy(p);
+        return st;
+    };
+    if (n_taps > 0) { // quantize_taps (fir.hpp:69-74)
+        std::vector<float> taps(n_taps * n_channels);
+        for (size_t k = 0; k < taps.size(); ++k)
+            taps[k] = static_cast<float>(coeff_values[k]);
+        if (cudaMalloc(&p->d_taps, taps.size() * sizeof(float)) != cudaSuccess ||
+            cudaMemcpy(p->d_taps, taps.data(), taps.size() * sizeof(float),
+                       cudaMemcpyHostToDevice) != cudaSuccess)
+            return cleanup(fail(PPFG_CUDA_ERROR, "ppfg_plan_create: tap upload failed"));
+    }
+    if (p->L >= 1) {
+        const auto tw = host_twiddles(n_channels);
+        if (cudaMalloc(&p->d_tw, tw.size() * sizeof(float2)) != cudaSuccess ||
+            cudaMemcpy(p->d_tw, tw.data(), tw.size() * sizeof(float2), cudaMemcpyHostToDevice) !=
+                cudaSuccess)
+            return cleanup(fail(PPFG_CUDA_ERROR, "ppfg_plan_create: twiddle upload failed"));
+    } else if (p->L < 0) {
+        const auto r = host_roots(n_channels);
+        if (cudaMalloc(&p->d_roots, r.size() * sizeof(double2)) != cudaSuccess ||
+            cudaMemcpy(p->d_roots, r.data(), r.size() * sizeof(double2),
+                       cudaMemcpyHostToDevice) != cudaSuccess)
+            return cleanup(fail(PPFG_CUDA_ERROR, "ppfg_plan_create: root upload failed"));
+    }
+    if (cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&p->s_d2h, cudaStreamNonBlocking) != cudaSuccess)
+        return cleanup(fail(PPFG_CUDA_ERROR, "ppfg_plan_create: stream creation failed"));
+    p->own_stream = true;
+    for (int i = 0; i < 2; ++i) {
+        if (cudaEventCreateWithFlags(&p->ev_h2d[i], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&p->ev_comp[i], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&p->ev_d2h[i], cudaEventDisableTiming) != cudaSuccess)
+            return cleanup(fail(PPFG_CUDA_ERROR, "ppfg_plan_create: event creation failed"));
+    }
+    if (n_taps > 0 && p->L >= 0) {
+        const bool exact = !(flags & PPFG_FAST);
+        for (const auto& e : fused_table()) {
+            if (e.L == p->L && e.T == static_cast<int>(n_taps) && e.exact == exact) {
+                p->fused = &e;
+                break;
+            }
+        }
+    }
+    *plan = p;
+    return PPFG_OK;
+}
+
+int ppfg_plan_destroy(ppfg_plan p) {
+    if (!p)
+        return PPFG_OK;
+    DeviceGuard dg(p->device);
+    if (p->stream)
+        cudaStreamSynchronize(p->stream);
+    cudaFree(p->d_taps);
+    cudaFree(p->d_tw);
+    cudaFree(p->d_roots);
+    for (int i = 0; i < 2; ++i) {
+        cudaFree(p->d_in[i]);
+        cudaFree(p->d_out[i]);
+        if (p->h_in[i])
+            cudaFreeHost(p->h_in[i]);
+        if (p->h_out[i])
+            cudaFreeHost(p->h_out[i]);
+        if (p->ev_h2d[i])
+            cudaEventDestroy(p->ev_h2d[i]);
+        if (p->ev_comp[i])
+            cudaEventDestroy(p->ev_comp[i]);
+        if (p->ev_d2h[i])
+            cudaEventDestroy(p->ev_d2h[i]);
+    }
+    if (p->own_stream) {
+        cudaStreamDestroy(p->stream);
+        cudaStreamDestroy(p->s_h2d);
+        cudaStreamDestroy(p->s_d2h);
+    }
+    delete p;
+    return PPFG_OK;
+}
+
+void* ppfg_plan_stream(ppfg_plan plan) { return plan ? plan->stream : nullptr; }
+
+int ppfg_fir_fft_kind(ppfg_plan p) {
+    if (!p || !p->fused || (p->flags & PPFG_UNFUSED))
+        return 0;
+    return p->fused->exact ? 2 : 1;
+}
+
+int ppfg_fir(ppfg_plan p, const void* in, uint64_t n_spectra_in, void* out, int mem,
+             void* cuda_stream) {
+    PPFG_TRY(check_fir_input(p, in, n_spectra_in, out));
+    if (in == out)
+        return fail(PPFG_CONFIG_ERROR, "fir: input and output must not alias");
+    return run(p, Op::Fir, in, n_spectra_in, out, mem, cuda_stream, p->T - 1);
+}
+
+// ppf_fir_reference's start-from-zero ordering (fir.hpp:138-145)
+int ppfg_fir_reference_order(ppfg_plan p, const void* in, uint64_t n_spectra_in, void* out,
+                             int mem, void* cuda_stream) {
+    PPFG_TRY(check_fir_input(p, in, n_spectra_in, out));
+    if (in == out)
+        return fail(PPFG_CONFIG_ERROR, "fir: input and output must not alias");
+    return run(p, Op::FirRef, in, n_spectra_in, out, mem, cuda_stream, p->T - 1);
+}
+
+int ppfg_channelize(ppfg_plan p, const void* in, uint64_t n_rows, void* out, int fft_fallback,
+                    int mem, void* cuda_stream) {
+    PPFG_TRY(check_plan(p));
+    if (n_rows == 0)
+        return PPFG_OK;
+    if (!in || !out)
+        return fail(PPFG_CONFIG_ERROR, "channelize_block: null buffer");
+    if (!is_pow2(p->C) && !fft_fallback)
+        return fail(PPFG_UNSUPPORTED_SIZE,
+                    "channelize_block: non-power-of-two channel count with fallback disabled");
+    return run(p, fft_fallback ? Op::Channelize : Op::ChannelizeNoFallback, in, n_rows, out, mem,
+               cuda_stream, 0);
+}
+
+int ppfg_fir_fft(ppfg_plan p, const void* in, uint64_t n_spectra_in, void* out, int mem,
+                 void* cuda_stream) {
+    PPFG_TRY(check_fir_input(p, in, n_spectra_in, out));
+    if (in == out)
+        return fail(PPFG_CONFIG_ERROR, "fir_fft: input and output must not alias");
+    return run(p, Op::FirFft, in, n_spectra_in, out, mem, cuda_stream, p->T - 1);
+}
+
+static int one_row(const void* in, uint64_t n, void* out, bool fallback, const char* who) {
+    if (n == 0)
+        return fail(PPFG_CONFIG_ERROR, std::string(who) + ": empty spectrum");
+    if (!fallback && !is_pow2(n))
+        return fail(PPFG_UNSUPPORTED_SIZE, "fft: size must be a power of two");
+    int dev = 0;
+    cudaGetDevice(&dev);
+    ppfg_plan p = nullptr;
+    PPFG_TRY(ppfg_plan_create(&p, n, 0, nullptr, 0, dev));
+    int rc;
+    if (fallback && is_pow2(n) && n > 1) { // force the naive path for dft_naive
+        DeviceGuard dg(p->device);
+        void* d = nullptr;
+        rc = cudaMalloc(&d, 2 * n * sizeof(float2)) == cudaSuccess ? PPFG_OK : PPFG_CUDA_ERROR;
+        if (rc == PPFG_OK) {
+            const auto r = host_roots(n);
+            double2* dr = nullptr;
+            cudaMalloc(&dr, n * sizeof(double2));
+            cudaMemcpy(dr, r.data(), n * sizeof(double2), cudaMemcpyHostToDevice);
+            cudaMemcpy(d, in, n * sizeof(float2), cudaMemcpyHostToDevice);
+            float2* din = static_cast<float2*>(d);
+            dft_naive_kernel<<<static_cast<unsigned>(cdiv(n, 256)), 256, 0, p->stream>>>(
+                din, din + n, static_cast<unsigned>(n), 1, dr);
+            rc = check_launch("dft_naive kernel");
+            cudaMemcpyAsync(out, din + n, n * sizeof(float2), cudaMemcpyDeviceToHost, p->stream);
+            cudaStreamSynchronize(p->stream);
+            cudaFree(dr);
+            cudaFree(d);
+        }
+    } else {
+        rc = ppfg_channelize(p, in, 1, out, fallback ? 1 : 0, PPFG_MEM_HOST, nullptr);
+    }
+    ppfg_plan_destroy(p);
+    return rc;
+}
+
+int ppfg_fft(const void* in, uint64_t n, void* out) { return one_row(in, n, out, false, "fft"); }
+int ppfg_dft_naive(const void* in, uint64_t n, void* out) {
+    return one_row(in, n, out, true, "dft_naive");
+}
+
+// ---------------------------------------------------------------- shards
+int ppfg_shard_range(uint64_t n_spectra_in, uint64_t n_taps, int rank, int world,
+                     uint64_t* in_begin, uint64_t* in_count, uint64_t* out_begin,
+                     uint64_t* out_count) {
+    if (world < 1 || rank < 0 || rank >= world || n_taps == 0)
+        return fail(PPFG_CONFIG_ERROR, "shard_range: bad rank/world/taps");
+    if (n_spectra_in < n_taps)
+        return fail(PPFG_INSUFFICIENT_HISTORY, "fir: need at least n_taps input spectra");
+    const uint64_t S_out = n_spectra_in - n_taps + 1;
+    const uint64_t base = S_out / world, extra = S_out % world;
+    const uint64_t r = static_cast<uint64_t>(rank);
+    const uint64_t ob = r * base + std::min<uint64_t>(r, extra);
+    const uint64_t oc = base + (r < extra ? 1 : 0);
+    *out_begin = ob;
+    *out_count = oc;
+    *in_begin = ob;
+    *in_count = oc > 0 ? oc + n_taps - 1 : 0;
+    return PPFG_OK;
+}
+
+int ppfg_multi_fir_fft(uint64_t n_channels, uint64_t n_taps, const double* coeff_values,
+                       uint32_t flags, const int* devices, int n_devices, const void* host_in,
+                       uint64_t n_spectra_in, void* host_out) {
+    if (n_devices < 1 || !devices)
+        return fail(PPFG_CONFIG_ERROR, "multi_fir_fft: need at least one device");
+    if (n_taps == 0 || n_spectra_in < n_taps)
+        return fail(n_taps == 0 ? PPFG_CONFIG_ERROR : PPFG_INSUFFICIENT_HISTORY,
+                    "fir: need at least n_taps input spectra");
+    std::vector<int> status(n_devices, PPFG_OK);
+    std::vector<std::string> msgs(n_devices);
+    std::vector<std::thread> pool;
+    const uint64_t row_bytes = n_channels * sizeof(float2);
+    for (int g = 0; g < n_devices; ++g) {
+        pool.emplace_back([&, g]() {
+            uint64_t ib, ic, ob, oc;
+            int st = ppfg_shard_range(n_spectra_in, n_taps, g, n_devices, &ib, &ic, &ob, &oc);
+            ppfg_plan p = nullptr;
+            if (st == PPFG_OK && oc > 0)
+                st = ppfg_plan_create(&p, n_channels, n_taps, coeff_values, flags, devices[g]);
+            if (st == PPFG_OK && oc > 0)
+                st = ppfg_fir_fft(p, static_cast<const char*>(host_in) + ib * row_bytes, ic,
+                                  static_cast<char*>(host_out) + ob * row_bytes, PPFG_MEM_HOST,
+                                  nullptr);
+            if (st != PPFG_OK)
+                msgs[g] = g_err;
+            ppfg_plan_destroy(p);
+            status[g] = st;
+        });
+    }
+    for (auto& t : pool)
+        t.join();
+    for (int g = 0; g < n_devices; ++g)
+        if (status[g] != PPFG_OK)
+            return fail(status[g], "shard " + std::to_string(g) + ": " + msgs[g]);
+    return PPFG_OK;
+}
+
+// ----------------------------------------------------------------- synth
+int ppfg_synth(uint64_t n_channels, uint64_t seed, uint64_t first_sample, uint64_t n_samples,
+               void* out, int mem, int device, void* cuda_stream) {
+    if (n_channels == 0)
+        return fail(PPFG_CONFIG_ERROR, "synth: n_channels must be >= 1");
+    const uint64_t M = 10 * n_channels, f10 = tone_f10(n_channels);
+    if (mem == PPFG_MEM_HOST) {
+        const auto tone = host_tone(n_channels);
+        float2* o = static_cast<float2*>(out);
+        for (uint64_t i = 0; i < n_samples; ++i) {
+            const uint64_t n = first_sample + i;
+            const float2 t = tone[(f10 * n) % M];
+            const uint64_t a = splitmix64(seed + (2 * n + 1) * kGolden);
+            const uint64_t b = splitmix64(seed + (2 * n + 2) * kGolden);
+            volatile float gr = static_cast<float>(irwin_hall4(a)) * kNoiseScale;
+            volatile float gi = static_cast<float>(irwin_hall4(b)) * kNoiseScale;
+            o[i] = make_float2(t.x + gr, t.y + gi);
+        }
+        return PPFG_OK;
+    }
+    DeviceGuard dg(device);
+    float2* dtone = nullptr;
+    {
+        auto& c = tone_cache();
+        std::lock_guard<std::mutex> lk(c.mu);
+        auto key = std::make_pair(device, n_channels);
+        auto it = c.dev.find(key);
+        if (it == c.dev.end()) {
+            const auto tone = host_tone(n_channels);
+            PPFG_CUDA(cudaMalloc(&dtone, tone.size() * sizeof(float2)));
+            PPFG_CUDA(cudaMemcpy(dtone, tone.data(), tone.size() * sizeof(float2),
+                                 cudaMemcpyHostToDevice));
+            c.dev[key] = dtone;
+        } else {
+            dtone = it->second;
+        }
+    }
+    if (n_samples == 0)
+        return PPFG_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    synth_kernel<<<static_cast<unsigned>(cdiv(n_samples, 256)), 256, 0, st>>>(
+        static_cast<float2*>(out), seed, first_sample, n_samples, f10, M, dtone);
+    return check_launch("synth kernel");
+}
+
+// ------------------------------------------------------- coefficient design
+// coeff.hpp:61-144 (same operations as the reference build, incl. the FMA GCC
+// contracts 1 - r*r into; pinned against the reference in tests)
+static double i0_series(double x) {
+    const double y = x * x * 0.25;
+    double term = 1.0, sum = 1.0;
+    for (int k = 1; k < 10000; ++k) {
+        term *= y / (static_cast<double>(k) * static_cast<double>(k));
+        sum += term;
+        if (term < sum * 1e-17)
+            break;
+    }
+    return sum;
+}
+
+int ppfg_generate_prototype(uint64_t n_channels, uint64_t n_taps, double beta,
+                            double cutoff_scale, double* out) {
+    if (n_channels == 0 || n_taps == 0)
+        return fail(PPFG_CONFIG_ERROR,
+                    "generate_prototype: n_channels and n_taps must be >= 1");
+    if (!(cutoff_scale > 0.0) || !std::isfinite(cutoff_scale))
+        return fail(PPFG_CONFIG_ERROR, "generate_prototype: cutoff_scale must be finite and > 0");
+    if (!(beta >= 0.0) || !std::isfinite(beta))
+        return fail(PPFG_CONFIG_ERROR, "window beta must be finite and >= 0");
+    if (beta > 700.0)
+        return fail(PPFG_DOMAIN_ERROR, "bessel_i0: |x| must be <= 700");
+    const uint64_t length = n_channels * n_taps;
+    std::vector<double> w(length, 1.0);
+    if (length > 1 && beta != 0.0) {
+        const double denom = i0_series(beta);
+        const double span = static_cast<double>(length - 1);
+        for (uint64_t k = 0; k < length; ++k) {
+            const double r = static_cast<double>(2 * static_cast<int64_t>(k) -
+                                                 static_cast<int64_t>(length - 1)) /
+                             span;
+            w[k] = i0_series(beta * std::sqrt(std::fma(-r, r, 1.0))) / denom;
+        }
+    }
+    const double step = M_PI * cutoff_scale / (2.0 * static_cast<double>(n_channels));
+    double sum = 0.0;
+    for (uint64_t k = 0; k < length; ++k) {
+        const double num = static_cast<double>(2 * static_cast<int64_t>(k) -
+                                               static_cast<int64_t>(length - 1));
+        const double x = num * step;
+        const double v = (x == 0.0 ? 1.0 : std::sin(x) / x) * w[k];
+        out[k] = v;
+        sum += v;
+    }
+    if (!std::isfinite(sum) || sum == 0.0)
+        return fail(PPFG_DEGENERATE_FILTER, "generate_prototype: coefficient sum vanished");
+    for (uint64_t k = 0; k < length; ++k)
+        out[k] /= sum;
+    return PPFG_OK;
+}
+
+} // extern "C"
+
+// ============================================================ streaming
+// Device-resident process_stream state (pipeline.hpp:43-200). The carried
+// history (carry_history, pipeline.hpp:55-73) stays on the device: each chunk
+// of newly completed spectra is uploaded right behind it, the fused kernel
+// runs over history ++ chunk, and the last T-1 spectra become the next history
+// (ping-pong buffers, no overlap hazards).
+struct ppfg_stream_s {
+    ppfg_plan plan = nullptr;
+    uint64_t block_spectra = 0;
+    bool fallback = true;
+    float2* d_buf[2] = {nullptr, nullptr};
+    float2* d_out = nullptr;
+    int cur = 0;
+    uint64_t cap_rows = 0;  // new rows per device chunk
+    uint64_t hist_rows = 0; // valid history rows at the front of d_buf[cur]
+    uint8_t byte_carry[8];
+    int byte_carry_n = 0;
+    std::vector<float2> sample_carry;
+    ppfg_stream_state st{};
+    uint64_t stream_offset = 0;
+};
+
+extern "C" {
+
+int ppfg_stream_open(ppfg_stream* out, ppfg_plan p, uint64_t block_spectra, int zero_prime,
+                     int fft_fallback) {
+    if (!out)
+        return fail(PPFG_CONFIG_ERROR, "stream_open: null stream pointer");
+    *out = nullptr;
+    PPFG_TRY(check_plan(p));
+    if (p->T == 0)
+        return fail(PPFG_CONFIG_ERROR, "config: n_taps must be >= 1");
+    if (block_spectra < p->T) // PpfConfig::validate, pipeline.hpp:33-34
+        return fail(PPFG_CONFIG_ERROR, "config: block_spectra must be >= n_taps");
+    DeviceGuard dg(p->device);
+    auto* s = new ppfg_stream_s();
+    s->plan = p;
+    s->block_spectra = block_spectra;
+    s->fallback = fft_fallback != 0;
+    const uint64_t row_bytes = p->C * sizeof(float2);
+    s->cap_rows = std::max<uint64_t>(1, std::min<uint64_t>(block_spectra, kChunkBytes / row_bytes));
+    const uint64_t buf_rows = s->cap_rows + p->T;
+    for (int i = 0; i < 2; ++i) {
+        if (cudaMalloc(&s->d_buf[i], buf_rows * row_bytes) != cudaSuccess) {
+            ppfg_stream_destroy(s);
+            return fail(PPFG_CUDA_ERROR, "stream_open: device allocation failed");
+        }
+    }
+    if (cudaMalloc(&s->d_out, buf_rows * row_bytes) != cudaSuccess) {
+        ppfg_stream_destroy(s);
+        return fail(PPFG_CUDA_ERROR, "stream_open: device allocation failed");
+    }
+    if (zero_prime) { // pipeline.hpp:110-111
+        s->hist_rows = p->T - 1;
+        if (s->hist_rows)
+            cudaMemset(s->d_buf[0], 0, s->hist_rows * row_bytes);
+    }
+    *out = s;
+    return PPFG_OK;
+}
+
+int ppfg_stream_push(ppfg_stream s, const void* bytes, uint64_t n, void* out, uint64_t out_cap,
+                     uint64_t* out_len) {
+    if (!s)
+        return fail(PPFG_CONFIG_ERROR, "stream_push: null stream");
+    ppfg_plan p = s->plan;
+    DeviceGuard dg(p->device);
+    const uint64_t C = p->C, T = p->T;
+    const uint64_t row_bytes = C * sizeof(float2);
+    *out_len = 0;
+    const uint8_t* data = static_cast<const uint8_t*>(bytes);
+    uint64_t avail = n;
+    // complete a sample split across pushes (pipeline.hpp:151-163)
+    if (s->byte_carry_n != 0 && avail) {
+        const uint64_t take = std::min<uint64_t>(8 - s->byte_carry_n, avail);
+        std::memcpy(s->byte_carry + s->byte_carry_n, data, take);
+        s->byte_carry_n += static_cast<int>(take);
+        data += take;
+        avail -= take;
+        if (s->byte_carry_n == 8) {
+            float2 z;
+            std::memcpy(&z, s->byte_carry, 8);
+            s->sample_carry.push_back(z);
+            s->byte_carry_n = 0;
+        }
+    }
+    const uint64_t full = avail / 8, tail = avail % 8;
+    const size_t old = s->sample_carry.size();
+    s->sample_carry.resize(old + full);
+    std::memcpy(s->sample_carry.data() + old, data, full * 8);
+    if (tail) {
+        std::memcpy(s->byte_carry, data + full * 8, tail);
+        s->byte_carry_n = static_cast<int>(tail);
+    }
+    s->stream_offset += n;
+
+    const uint64_t full_spectra = s->sample_carry.size() / C;
+    uint64_t done = 0;
+    char* o = static_cast<char*>(out);
+    while (done < full_spectra) {
+        const uint64_t rows = std::min(s->cap_rows, full_spectra - done);
+        float2* buf = s->d_buf[s->cur];
+        PPFG_CUDA(cudaMemcpyAsync(buf + s->hist_rows * C, s->sample_carry.data() + done * C,
+                                  rows * row_bytes, cudaMemcpyHostToDevice, p->stream));
+        const uint64_t total = s->hist_rows + rows;
+        s->st.bytes_in += rows * row_bytes;
+        if (total >= T) {
+            const uint64_t n_out = total - T + 1;
+            if (*out_len + n_out * row_bytes > out_cap)
+                return fail(PPFG_CONFIG_ERROR, "stream_push: output buffer too small");
+            if (s->fallback || is_pow2(C)) {
+                PPFG_TRY(launch_fir_fft(p, buf, total, s->d_out, p->stream));
+            } else {
+                return fail(PPFG_UNSUPPORTED_SIZE, "channelize_block: non-power-of-two channel "
+                                                   "count with fallback disabled");
+            }
+            PPFG_CUDA(cudaMemcpyAsync(o + *out_len, s->d_out, n_out * row_bytes,
+                                      cudaMemcpyDeviceToHost, p->stream));
+            *out_len += n_out * row_bytes;
+            s->st.spectra_processed += n_out;
+            s->st.bytes_out += n_out * row_bytes;
+        }
+        const uint64_t keep = std::min<uint64_t>(T - 1, total);
+        if (keep)
+            PPFG_CUDA(cudaMemcpyAsync(s->d_buf[s->cur ^ 1], buf + (total - keep) * C,
+                                      keep * row_bytes, cudaMemcpyDeviceToDevice, p->stream));
+        s->cur ^= 1;
+        s->hist_rows = keep;
+        done += rows;
+    }
+    s->sample_carry.erase(s->sample_carry.begin(),
+                          s->sample_carry.begin() + static_cast<std::ptrdiff_t>(done * C));
+    PPFG_CUDA(cudaStreamSynchronize(p->stream));
+    return PPFG_OK;
+}
+
+int ppfg_stream_close(ppfg_stream s, ppfg_stream_state* state) {
+    if (!s)
+        return fail(PPFG_CONFIG_ERROR, "stream_close: null stream");
+    if (s->byte_carry_n != 0) { // pipeline.hpp:190-192
+        g_err_offset = s->stream_offset - s->byte_carry_n;
+        const std::string m = "process_stream: stream truncated mid-sample at byte offset " +
+                              std::to_string(g_err_offset);
+        if (state)
+            *state = s->st;
+        return fail(PPFG_DECODE_ERROR, m);
+    }
+    s->st.dropped_samples += s->sample_carry.size(); // pipeline.hpp:194
+    s->sample_carry.clear();
+    if (state)
+        *state = s->st;
+    return PPFG_OK;
+}
+
+int ppfg_stream_destroy(ppfg_stream s) {
+    if (!s)
+        return PPFG_OK;
+    DeviceGuard dg(s->plan->device);
+    cudaFree(s->d_buf[0]);
+    cudaFree(s->d_buf[1]);
+    cudaFree(s->d_out);
+    delete s;
+    return PPFG_OK;
+}
+
+int ppfg_process_stream(ppfg_plan p, uint64_t block_spectra, int zero_prime, int fft_fallback,
+                        ppfg_read_fn read, void* read_ctx, ppfg_write_fn write, void* write_ctx,
+                        ppfg_stream_state* state) {
+    if (state)
+        *state = ppfg_stream_state{};
+    PPFG_TRY(check_plan(p));
+    if (!read || !write)
+        return fail(PPFG_CONFIG_ERROR, "process_stream: null callback");
+    ppfg_stream s = nullptr;
+    PPFG_TRY(ppfg_stream_open(&s, p, block_spectra, zero_prime, fft_fallback));
+    const uint64_t row_bytes = p->C * 8;
+    const uint64_t io = block_spectra * row_bytes; // pipeline.hpp:113
+    std::vector<char> in(io);
+    std::vector<char> outb((block_spectra + 2) * row_bytes + row_bytes);
+    int rc = PPFG_OK;
+    for (;;) {
+        const int64_t got = read(read_ctx, in.data(), io);
+        if (got < 0) {
+            g_err_offset = s->stream_offset;
+            rc = fail(PPFG_DECODE_ERROR, "process_stream: source read failed at byte offset " +
+                                             std::to_string(s->stream_offset));
+            break;
+        }
+        if (got == 0)
+            break;
+        uint64_t out_len = 0;
+        rc = ppfg_stream_push(s, in.data(), static_cast<uint64_t>(got), outb.data(), outb.size(),
+                              &out_len);
+        if (rc != PPFG_OK)
+            break;
+        if (out_len && write(write_ctx, outb.data(), out_len) != 0) {
+            rc = fail(PPFG_IO_ERROR, "process_stream: sink write failed");
+            break;
+        }
+        if (static_cast<uint64_t>(got) < io)
+            break;
+    }
+    if (rc == PPFG_OK)
+        rc = ppfg_stream_close(s, state);
+    else if (state)
+        *state = s->st;
+    ppfg_stream_destroy(s);
+    return rc;
+}
+
+} // extern "C"

@@ -1,0 +1,321 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle on the same
+seeded inputs and against the reference's golden vectors.
+
+Bars (SURVEY §8c / BASELINE.json north_star):
+  * FIR (K1), FFT (K2), dft_naive (K4), fused EXACT (K3 fp64) and streaming:
+    bit-identical to the reference.
+  * fused FAST (K3 fp32 FIR): max|err|/RMS <= 1e-5 * log2(C) (north star).
+"""
+import io
+
+import numpy as np
+import pytest
+
+from conftest import bits, max_err_over_rms, uniform
+
+pytestmark = pytest.mark.gpu
+
+
+def ppf_mod():
+    from paper_1411_3656_b200 import ppf
+    return ppf
+
+
+# ---------------------------------------------------------------- FIR (K1)
+def test_fir_golden_bitwise(cuda, golden):
+    ppf = ppf_mod()
+    for i in range(int(golden["n_fir"])):
+        C, T = int(golden[f"fir{i}_C"]), int(golden[f"fir{i}_T"])
+        x, c = golden[f"fir{i}_x"].view(np.complex64), golden[f"fir{i}_coeffs"]
+        with ppf.Plan(C, T, c) as p:
+            assert np.array_equal(bits(p.fir(x)), bits(golden[f"fir{i}_y"])), (C, T)
+            assert np.array_equal(bits(p.fir_reference(x)), bits(golden[f"fir{i}_y_ref"])), (C, T)
+
+
+@pytest.mark.parametrize("C", [1, 2, 3, 8, 64, 100, 256, 1024, 4096])
+@pytest.mark.parametrize("T", [1, 2, 4, 7, 8, 16, 17, 32, 64])
+def test_fir_bitwise_vs_oracle(cuda, port, C, T):
+    ppf = ppf_mod()
+    rng = np.random.default_rng(C * 1000 + T)
+    S = T + int(rng.integers(0, 40)) + (3000 if C <= 64 else 0)
+    x = uniform(rng, S * C)
+    coeffs = port.generate_prototype(C, T, 9.0)
+    with ppf.Plan(C, T, coeffs) as p:
+        got = p.fir(x)
+    assert got.shape == (S - T + 1, C)
+    assert np.array_equal(bits(got), bits(port.fir(x, C, T, coeffs)))
+
+
+def test_fir_errors(cuda):
+    ppf = ppf_mod()
+    rng = np.random.default_rng(113)
+    c = ppf.generate_prototype(8, 4)
+    with pytest.raises(ppf.insufficient_history_error):   # fir_test.cpp:129-134
+        ppf.ppf_fir_reference(uniform(rng, 8 * 3), c)
+    with pytest.raises(ppf.config_error):                 # fir_test.cpp:122-127
+        ppf.ppf_fir_optimized(uniform(rng, 8 * 16), ppf.generate_prototype(16, 4), n_channels=8)
+    with pytest.raises(ppf.config_error):
+        ppf.ppf_fir_optimized(uniform(rng, 8 * 16), c, workers=0)
+
+
+def test_fir_properties(cuda):
+    """fir_test.cpp:171-257: shift equivariance and channel independence are exact;
+    a finite impulse response touches exactly T spectra of one channel."""
+    ppf = ppf_mod()
+    rng = np.random.default_rng(149)
+    C, T, S = 8, 4, 24
+    c = ppf.generate_prototype(C, T)
+    x = uniform(rng, S * C)
+    base = ppf.ppf_fir_optimized(x, c)
+    moved = ppf.ppf_fir_optimized(np.concatenate([uniform(rng, C), x]), c)
+    assert np.array_equal(bits(moved[1:]), bits(base))
+    masked = x.copy().reshape(S, C)
+    masked[:, 3] = 0
+    got = ppf.ppf_fir_optimized(masked, c)
+    assert np.all(got[:, 3] == 0)
+    keep = [k for k in range(C) if k != 3]
+    assert np.array_equal(bits(got[:, keep]), bits(base[:, keep]))
+    imp = np.zeros((30, 8), np.complex64)
+    imp[14, 5] = 0.5 - 2.0j
+    coeffs = ppf.FilterCoefficients(8, 6, rng.uniform(0.25, 1.75, 48))
+    y = ppf.ppf_fir_optimized(imp, coeffs)
+    nz = y != 0
+    assert nz[:, [k for k in range(8) if k != 5]].sum() == 0 and nz[:, 5].sum() == 6
+
+
+# ---------------------------------------------------------------- FFT (K2/K4)
+def test_fft_golden_bitwise(cuda, golden):
+    ppf = ppf_mod()
+    for n in golden["fft_sizes"]:
+        n = int(n)
+        got = ppf.channelize_block(golden[f"fft{n}_x"].view(np.complex64), n)
+        assert np.array_equal(bits(got), bits(golden[f"fft{n}_y"])), n
+    for n in golden["dft_sizes"]:
+        n = int(n)
+        got = ppf.channelize_block(golden[f"dft{n}_x"].view(np.complex64), n)
+        assert np.array_equal(bits(got), bits(golden[f"dft{n}_y"])), n
+
+
+@pytest.mark.parametrize("L", list(range(0, 17)))
+def test_fft_bitwise_vs_oracle(cuda, port, L):
+    ppf = ppf_mod()
+    n = 1 << L
+    rng = np.random.default_rng(L)
+    rows = max(3, (1 << 16) // n) + 1
+    x = uniform(rng, rows * n)
+    got = ppf.channelize_block(x, n)
+    assert np.array_equal(bits(got), bits(port.channelize(x, n)))
+
+
+def test_fft_api_semantics(cuda, port):
+    """dft_test.cpp:72-123, 125-197."""
+    ppf = ppf_mod()
+    assert ppf.fft(np.array([0.25 - 1.5j], np.complex64))[0] == np.complex64(0.25 - 1.5j)
+    d = np.zeros(8, np.complex64)
+    d[0] = 1
+    assert np.allclose(ppf.fft(d), 1.0)
+    with pytest.raises(ppf.unsupported_size_error):
+        ppf.fft(np.ones(12, np.complex64))
+    x = uniform(np.random.default_rng(241), 6 * 4)
+    with pytest.raises(ppf.unsupported_size_error):
+        ppf.channelize_block(x, 6, fft_fallback=False)
+    assert ppf.channelize_block(np.zeros(0, np.complex64), 4).size == 0
+    for n in (3, 12, 100):
+        x = uniform(np.random.default_rng(n), n)
+        assert np.array_equal(bits(ppf.dft_naive(x)), bits(port.dft_naive(x)))
+    for n in (1, 2, 64, 512):
+        x = uniform(np.random.default_rng(n), n)
+        assert np.array_equal(bits(ppf.fft(x)), bits(port.fft(x)))
+
+
+def test_channelize_in_place_device(cuda, port):
+    import torch
+    ppf = ppf_mod()
+    for n in (6, 64, 1024, 32768):
+        rng = np.random.default_rng(n)
+        x = uniform(rng, 17 * n)
+        t = torch.from_numpy(x.copy()).to(cuda)
+        with ppf.Plan(n) as p:
+            p.channelize(t, out=t)
+        torch.cuda.synchronize()
+        assert np.array_equal(bits(t.cpu().numpy()), bits(port.channelize(x, n))), n
+
+
+# ---------------------------------------------------------------- fused (K3)
+def test_fused_golden_exact(cuda, golden):
+    ppf = ppf_mod()
+    for i in range(int(golden["n_ff"])):
+        C, T = int(golden[f"ff{i}_C"]), int(golden[f"ff{i}_T"])
+        with ppf.Plan(C, T, golden[f"ff{i}_coeffs"], flags=ppf.EXACT) as p:
+            got = p.fir_fft(golden[f"ff{i}_x"].view(np.complex64))
+        assert np.array_equal(bits(got), bits(golden[f"ff{i}_y"])), (C, T)
+
+
+@pytest.mark.parametrize("C,T", [(512, 8), (1024, 8), (64, 8), (256, 4), (2048, 8), (8192, 8),
+                                 (1024, 4), (1024, 16), (512, 16), (128, 8)])
+@pytest.mark.parametrize("flags", ["exact", "fast"])
+def test_fused_vs_oracle(cuda, port, C, T, flags):
+    ppf = ppf_mod()
+    rng = np.random.default_rng(C + T)
+    S = T - 1 + 148 * 8 * 3 + int(rng.integers(0, 50))   # several batches per CTA + ragged tail
+    if C >= 2048:
+        S = T - 1 + 700
+    x = ppf.synth(C, S * C, seed=C * 31 + T)
+    coeffs = port.generate_prototype(C, T, 9.0)
+    want = port.fir_fft(x, C, T, coeffs).view(np.complex64)
+    with ppf.Plan(C, T, coeffs, flags=ppf.EXACT if flags == "exact" else ppf.FAST) as p:
+        got = p.fir_fft(x)
+        kind = p.kind
+    assert got.shape == (S - T + 1, C)
+    if flags == "exact" or kind == 0:
+        assert np.array_equal(bits(got), bits(want)), f"kind={kind}"
+    else:
+        err = max_err_over_rms(got, want)
+        assert err <= 1e-5 * np.log2(C), err
+
+
+@pytest.mark.parametrize("S_extra", [0, 1, 2, 7, 8, 9, 100])
+def test_fused_small_and_ragged(cuda, port, S_extra):
+    """n_spectra_out = 1 and tails that do not fill a batch (SURVEY §7 hard part 7)."""
+    ppf = ppf_mod()
+    for C, T, flags in [(512, 8, ppf.EXACT), (1024, 8, ppf.FAST), (512, 8, ppf.FAST)]:
+        S = T + S_extra
+        x = uniform(np.random.default_rng(S_extra), S * C)
+        coeffs = port.generate_prototype(C, T, 9.0)
+        want = port.fir_fft(x, C, T, coeffs)
+        with ppf.Plan(C, T, coeffs, flags=flags) as p:
+            got = p.fir_fft(x)
+        if flags == ppf.EXACT:
+            assert np.array_equal(bits(got), bits(want))
+        else:
+            assert max_err_over_rms(got, want) <= 1e-5 * np.log2(C)
+
+
+def test_fused_device_resident_torch(cuda, port):
+    import torch
+    ppf = ppf_mod()
+    C, T, S = 1024, 8, 5000
+    with ppf.Plan(C, T, port.generate_prototype(C, T, 9.0), flags=ppf.FAST) as p:
+        x = torch.empty((S, C), dtype=torch.complex64, device=cuda)
+        ppf.synth(C, S * C, seed=5, out=x)
+        y = p.fir_fft(x)
+        torch.cuda.synchronize()
+        host = ppf.synth(C, S * C, seed=5)
+        assert np.array_equal(bits(x.cpu().numpy()), bits(host))   # device == host generator
+        want = port.fir_fft(host, C, T, port.generate_prototype(C, T, 9.0))
+        assert max_err_over_rms(y.cpu().numpy(), want) <= 1e-5 * np.log2(C)
+
+
+def test_unfused_flag_is_bitwise_exact(cuda, port):
+    ppf = ppf_mod()
+    C, T, S = 1024, 8, 3000
+    x = ppf.synth(C, S * C, seed=9)
+    c = port.generate_prototype(C, T, 9.0)
+    with ppf.Plan(C, T, c, flags=ppf.UNFUSED) as p:
+        assert p.kind == 0
+        assert np.array_equal(bits(p.fir_fft(x)), bits(port.fir_fft(x, C, T, c)))
+
+
+# ---------------------------------------------------------------- streaming
+def test_stream_golden_and_block_invariance(cuda, golden, port):
+    """pipeline_test.cpp:156-170 and acceptance criterion 6: byte-identical
+    output for any block size, equal to the reference's bytes."""
+    ppf = ppf_mod()
+    src = golden["stream_x"].tobytes()
+    for bs in (8, 100, 999, 4096):
+        sink = io.BytesIO()
+        st = ppf.process_stream(8, 8, io.BytesIO(src), sink, block_spectra=bs)
+        assert sink.getvalue() == golden["stream_y"].tobytes(), bs
+        assert [st.spectra_processed, st.bytes_in, st.bytes_out, st.dropped_samples] == \
+            [int(v) for v in golden["stream_state"]]
+    sink = io.BytesIO()
+    ppf.process_stream(8, 8, io.BytesIO(src), sink, block_spectra=64, zero_prime=True)
+    assert sink.getvalue() == golden["stream_zp_y"].tobytes()
+
+
+def test_stream_arbitrary_pushes_equal_one_shot(cuda, port):
+    ppf = ppf_mod()
+    C, T = 1024, 8
+    rng = np.random.default_rng(20140606)
+    x = ppf.synth(C, 3000 * C, seed=11)
+    raw = x.tobytes()
+    coeffs = ppf.generate_prototype(C, T)
+    want = port.fir_fft(x, C, T, coeffs.values).tobytes()
+    for flags in (ppf.EXACT, ppf.FAST):
+        with ppf.Plan(C, T, coeffs, flags=flags) as p:
+            s = ppf.Stream(p, block_spectra=512)
+            out = b""
+            pos = 0
+            while pos < len(raw):
+                n = int(rng.integers(1, 3 * 8 * C))
+                out += s.push(raw[pos:pos + n])
+                pos += n
+            st = s.close()
+            s.destroy()
+        assert st.spectra_processed == 3000 - T + 1
+        if flags == ppf.EXACT:
+            assert out == want
+        else:
+            assert max_err_over_rms(np.frombuffer(out, np.complex64),
+                                    np.frombuffer(want, np.complex64)) <= 1e-5 * np.log2(C)
+
+
+def test_stream_errors(cuda):
+    ppf = ppf_mod()
+    rng = np.random.default_rng(349)
+    raw = uniform(rng, 4 * 6).tobytes() + b"\x01\x02\x03"
+    with pytest.raises(ppf.decode_error) as e:       # pipeline_test.cpp:219-233
+        ppf.process_stream(4, 2, io.BytesIO(raw), io.BytesIO(), block_spectra=4)
+    assert e.value.byte_offset == 6 * 4 * 8
+
+    class Failing:
+        def write(self, b):
+            raise OSError("full")
+    with pytest.raises(ppf.io_error):                 # pipeline_test.cpp:251-258
+        ppf.process_stream(4, 2, io.BytesIO(uniform(rng, 32).tobytes()), Failing(),
+                           block_spectra=4)
+    with pytest.raises(ppf.config_error):             # pipeline_test.cpp:270-276
+        ppf.process_stream(8, 4, io.BytesIO(b""), io.BytesIO(), block_spectra=2)
+    st = ppf.process_stream(4, 3, io.BytesIO(uniform(rng, 8).tobytes()), io.BytesIO(),
+                            block_spectra=16)
+    assert st.spectra_processed == 0                  # pipeline_test.cpp:138-145
+
+
+# ---------------------------------------------------------------- shards / synth
+def test_shards_reassemble_the_one_shot(cuda, port):
+    """each shard = its segment + (T-1) halo, no collective; the
+    concatenated shard outputs equal the one-shot output bit for bit."""
+    ppf = ppf_mod()
+    C, T, S = 1024, 16, 4000
+    x = ppf.synth(C, S * C, seed=2).reshape(S, C)
+    c = ppf.generate_prototype(C, T)
+    want = port.fir_fft(x, C, T, c.values).view(np.complex64).reshape(-1, C)
+    for world in (1, 2, 3, 8):
+        parts = []
+        with ppf.Plan(C, T, c) as p:
+            for r in range(world):
+                ib, ic, ob, oc = ppf.shard_range(S, T, r, world)
+                parts.append(p.fir_fft(x[ib:ib + ic]))
+        assert np.array_equal(bits(np.concatenate(parts)), bits(want))
+    got = ppf.multi_fir_fft(x, c, devices=[0, 0])
+    assert np.array_equal(bits(got), bits(want))
+
+
+def test_host_pipeline_pinned_and_pageable(cuda, port):
+    """ppfg_fir_fft with host buffers: multi-chunk double-buffered pipeline,
+    pinned (torch pin_memory) and pageable (numpy) inputs give the same bytes."""
+    import torch
+    ppf = ppf_mod()
+    C, T = 1024, 8
+    S = (64 << 20) // (C * 8) * 2 + 777  # > 2 chunks of 64 MiB
+    c = ppf.generate_prototype(C, T)
+    x = ppf.synth(C, S * C, seed=4).reshape(S, C)
+    with ppf.Plan(C, T, c, flags=ppf.EXACT) as p:
+        a = p.fir_fft(x)
+        xp = torch.from_numpy(x).pin_memory()
+        b = p.fir_fft(xp)
+    assert np.array_equal(bits(a), bits(b.numpy()))
+    head = port.fir_fft(x[:3000], C, T, c.values)
+    assert np.array_equal(bits(a[:3000 - T + 1]), bits(head))
+    tail = port.fir_fft(x[-3000:], C, T, c.values)
+    assert np.array_equal(bits(a[-(3000 - T + 1):]), bits(tail))
