@@ -14,8 +14,9 @@
  * plan exactly as quantize_taps does (fir.hpp:69-74).
  *
  * Memory kinds: PPFG_MEM_DEVICE calls take device pointers, enqueue on the
- * given cudaStream_t (NULL = the plan's stream) and return without
- * synchronising. PPFG_MEM_HOST calls take host pointers (pinned or pageable),
+ * given cudaStream_t (NULL = the plan's own non-blocking stream; pass
+ * cudaStreamLegacy, (void*)1, for the legacy default stream) and return
+ * without synchronising. PPFG_MEM_HOST calls take host pointers (pinned or pageable),
  * run a chunked H2D -> kernel -> D2H pipeline and return when the output is in
  * host memory (the reference's synchronous contract, fir.hpp:158).
  *

@@ -42,6 +42,59 @@ PPFG_DEV void bfly(float2& lo, float2& hi, const float2 w) {
     lo.y = __fadd_rn(lo.y, ti);
 }
 
+// ---- packed FP32x2 (sm_100a FFMA2/FMUL2/FADD2) --------------------------------------
+// Each lane of a .f32x2 op rounds exactly like the scalar op, so these are
+// bit-identical to the scalar reference arithmetic at half the instructions.
+// A pair whose two halves are the same scalar compiles to the broadcast
+// operand form (R.F32), so "scalar x pair" costs no extra move.
+PPFG_DEV unsigned long long pk2(float a, float b) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+PPFG_DEV float2 upk2(unsigned long long r) {
+    float2 v;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+    return v;
+}
+PPFG_DEV float2 fma2(float2 a, float2 b, float2 c) {
+    unsigned long long d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;"
+        : "=l"(d)
+        : "l"(pk2(a.x, a.y)), "l"(pk2(b.x, b.y)), "l"(pk2(c.x, c.y)));
+    return upk2(d);
+}
+PPFG_DEV float2 mul2(float2 a, float2 b) {
+    unsigned long long d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pk2(a.x, a.y)), "l"(pk2(b.x, b.y)));
+    return upk2(d);
+}
+PPFG_DEV float2 add2(float2 a, float2 b) {
+    unsigned long long d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pk2(a.x, a.y)), "l"(pk2(b.x, b.y)));
+    return upk2(d);
+}
+PPFG_DEV float2 sub2(float2 a, float2 b) {
+    unsigned long long d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pk2(a.x, a.y)), "l"(pk2(b.x, b.y)));
+    return upk2(d);
+}
+// scalar s times pair b (+ c)
+PPFG_DEV float2 fma2s(float s, float2 b, float2 c) { return fma2(make_float2(s, s), b, c); }
+PPFG_DEV float2 mul2s(float s, float2 b) { return mul2(make_float2(s, s), b); }
+
+// The same butterfly on packed pairs with w4 = (wr, wi, -wi, wr):
+//   m = bi * (-wi, wr)            -> (-(bi*wi), bi*wr)    [RN each lane]
+//   t = br * (wr, wi) + m         -> (fma(br,wr,-(bi*wi)), fma(br,wi,bi*wr))
+//   hi = lo - t; lo = lo + t
+// 4 packed instructions (FMUL2, FFMA2, 2x FADD2) for the reference's 8.
+PPFG_DEV void bfly2(float2& lo, float2& hi, const float4 w) {
+    const float2 m = mul2s(hi.y, make_float2(w.z, w.w));
+    const float2 t = fma2s(hi.x, make_float2(w.x, w.y), m);
+    hi = sub2(lo, t);
+    lo = add2(lo, t);
+}
+
 // ---- mbarrier / bulk-copy (TMA 1-D) PTX wrappers --------------------------------
 PPFG_DEV uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));

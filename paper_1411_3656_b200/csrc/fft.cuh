@@ -25,8 +25,11 @@
 
 namespace ppfg {
 
+// Twiddles are stored as float4 (wr, wi, -wi, wr) — the reference's f32 table
+// entry tw[h-1+j] (dft.hpp:93-96) plus the swizzled copy the packed butterfly
+// (bfly2) consumes.
 template <bool TW_SMEM>
-PPFG_DEV float2 tw_load(const float2* p) {
+PPFG_DEV float4 tw_load(const float4* p) {
     if constexpr (TW_SMEM)
         return *p;
     else
@@ -35,21 +38,41 @@ PPFG_DEV float2 tw_load(const float2* p) {
 
 // Stages for label bits [LO, LO+W), high bit first. v[k] has label fixed|k<<LO.
 template <int L, int LO, int W, bool TW_SMEM>
-PPFG_DEV void fft_stages(float2 (&v)[1 << W], unsigned fixed, const float2* __restrict__ tw) {
+PPFG_DEV void fft_stages(float2 (&v)[1 << W], unsigned fixed, const float4* __restrict__ tw) {
 #pragma unroll
     for (int bb = W - 1; bb >= 0; --bb) {
         const int b = LO + bb;
         const int s = L - b;
         const unsigned half = 1u << (s - 1);
         const unsigned jf = (s > 1) ? (__brev(fixed >> (b + 1)) >> (33 - s)) : 0u;
-        const float2* twb = tw + (half - 1) + jf;
+        const float4* twb = tw + (half - 1) + jf;
 #pragma unroll
         for (int k = 0; k < (1 << W); ++k) {
             if (k & (1 << bb))
                 continue;
             const unsigned jk = crev((static_cast<unsigned>(k) << LO) >> (b + 1), s - 1);
-            const float2 w = tw_load<TW_SMEM>(twb + jk);
-            bfly(v[k], v[k | (1 << bb)], w);
+            const float4 w = tw_load<TW_SMEM>(twb + jk);
+            bfly2(v[k], v[k | (1 << bb)], w);
+        }
+    }
+}
+
+// The first RLOG stages (label bits L-1 .. L-RLOG) on a thread's R values
+// whose labels are j + k*N/R: their twiddle index j_f is 0, so every thread
+// needs exactly tw[0 .. R-2], passed in registers (twr).
+template <int L, int RLOG>
+PPFG_DEV void fft_prestages(float2 (&v)[1 << RLOG], const float4 (&twr)[RLOG > 0 ? (1 << RLOG) - 1 : 1]) {
+#pragma unroll
+    for (int bb = RLOG - 1; bb >= 0; --bb) {
+        const int b = L - RLOG + bb;
+        const int s = L - b;
+        const int half = 1 << (s - 1);
+#pragma unroll
+        for (int k = 0; k < (1 << RLOG); ++k) {
+            if (k & (1 << bb))
+                continue;
+            const unsigned jk = crev((static_cast<unsigned>(k) << (L - RLOG)) >> (b + 1), s - 1);
+            bfly2(v[k], v[k | (1 << bb)], twr[half - 1 + jk]);
         }
     }
 }
@@ -67,12 +90,12 @@ struct FftSchedule {
 //   FIRST_GLOBAL: this (top) pass reads natural-order input rows from global.
 //   FINAL       : this (bit-0) pass writes natural-order bins to global.
 // map(r) gives the global row of tile row r, or -1 for a padding row.
-template <int L, int LO, int W, bool FIRST_GLOBAL, bool FINAL, bool TW_SMEM, int NT, class RowMap>
 // gin/gout may alias (in-place channelize): every row is fully read before it is
 // written, with a barrier in between for multi-pass transforms.
+template <int L, int LO, int W, bool FIRST_GLOBAL, bool FINAL, bool TW_SMEM, int NT, class RowMap>
 PPFG_DEV void fft_tile_pass(const float2* gin, float2* gout,
                             float2* __restrict__ tile, unsigned row_stride, int rows,
-                            const RowMap& map, const float2* __restrict__ tw) {
+                            const RowMap& map, const float4* __restrict__ tw, int tid) {
     constexpr int N = 1 << L;
     constexpr int E = 1 << W;
     constexpr int HI = LO + W - 1;
@@ -80,7 +103,7 @@ PPFG_DEV void fft_tile_pass(const float2* gin, float2* gout,
     static_assert(!FIRST_GLOBAL || HI == L - 1, "a global-source pass must be the top pass");
     static_assert(!FINAL || LO == 0, "the final pass ends at label bit 0");
     const int units = rows * U;
-    for (int unit = threadIdx.x; unit < units; unit += NT) {
+    for (int unit = tid; unit < units; unit += NT) {
         const int r = unit / U;
         const unsigned u = static_cast<unsigned>(unit % U);
         unsigned fixed;
@@ -123,23 +146,31 @@ PPFG_DEV void fft_tile_pass(const float2* gin, float2* gout,
 
 // The passes covering label bits [0, LREM) of an N = 2^L transform (the top
 // L - LREM bits were already done, e.g. in the fused kernel's FIR threads).
+// `tid` is the thread's index among the NT threads running the passes and
+// `sync` the barrier between passes (__syncthreads, or a named barrier when
+// only the FFT warps of a warp-specialised CTA take part).
 template <int L, int LREM, int W, bool FIRST_GLOBAL, bool TW_SMEM, int NT, int I = 0>
 struct FftPasses {
     using S = FftSchedule<LREM, W>;
     static constexpr int WI = S::width(I);
     static constexpr int LO = S::lo(I);
     static constexpr bool FINAL = (I == S::NP - 1);
-    template <class RowMap>
+    template <class RowMap, class Sync>
     PPFG_DEV static void run(const float2* gin, float2* gout, float2* tile, unsigned row_stride,
-                             int rows, const RowMap& map, const float2* tw) {
+                             int rows, const RowMap& map, const float4* tw, int tid,
+                             const Sync& sync) {
         fft_tile_pass<L, LO, WI, FIRST_GLOBAL && I == 0, FINAL, TW_SMEM, NT>(
-            gin, gout, tile, row_stride, rows, map, tw);
+            gin, gout, tile, row_stride, rows, map, tw, tid);
         if constexpr (!FINAL) {
-            __syncthreads();
-            FftPasses<L, LREM, W, FIRST_GLOBAL, TW_SMEM, NT, I + 1>::run(gin, gout, tile,
-                                                                          row_stride, rows, map, tw);
+            sync();
+            FftPasses<L, LREM, W, FIRST_GLOBAL, TW_SMEM, NT, I + 1>::run(
+                gin, gout, tile, row_stride, rows, map, tw, tid, sync);
         }
     }
+};
+
+struct SyncCta {
+    PPFG_DEV void operator()() const { __syncthreads(); }
 };
 
 struct LinearRows {
@@ -154,23 +185,24 @@ struct LinearRows {
 template <int L, int W, bool TW_SMEM, int NT>
 __global__ void __launch_bounds__(NT) fft_rows_kernel(const float2* in, float2* out,
                                                       long long n_rows,
-                                                      const float2* __restrict__ tw_g) {
+                                                      const float4* __restrict__ tw_g) {
     constexpr int N = 1 << L;
     constexpr int RB = (NT << W) / N > 0 ? (NT << W) / N : 1;
-    extern __shared__ float2 smem[];
-    float2* tw_s = smem;
-    float2* tile = smem + (TW_SMEM ? ((N + 1) & ~1) : 0);
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    float4* tw_s = reinterpret_cast<float4*>(smem_raw);
+    float2* tile = reinterpret_cast<float2*>(smem_raw + (TW_SMEM ? sizeof(float4) * N : 0));
     if constexpr (TW_SMEM) {
         for (int i = threadIdx.x; i < N - 1; i += NT)
             tw_s[i] = tw_g[i];
         __syncthreads();
     }
-    const float2* tw = TW_SMEM ? tw_s : tw_g;
+    const float4* tw = TW_SMEM ? tw_s : tw_g;
     constexpr unsigned stride = sw_row_stride(N);
     for (long long row0 = static_cast<long long>(blockIdx.x) * RB; row0 < n_rows;
          row0 += static_cast<long long>(gridDim.x) * RB) {
         FftPasses<L, L, W, true, TW_SMEM, NT>::run(in, out, tile, stride, RB,
-                                                   LinearRows{row0, n_rows}, tw);
+                                                   LinearRows{row0, n_rows}, tw,
+                                                   static_cast<int>(threadIdx.x), SyncCta{});
         __syncthreads();
     }
 }
@@ -180,8 +212,8 @@ constexpr size_t fft_rows_smem_bytes() {
     constexpr int N = 1 << L;
     constexpr int RB = (NT << W) / N > 0 ? (NT << W) / N : 1;
     constexpr bool multipass = FftSchedule<L, W>::NP > 1;
-    return sizeof(float2) * ((TW_SMEM ? ((N + 1) & ~1) : 0) +
-                             (multipass ? static_cast<size_t>(RB) * sw_row_stride(N) : 0));
+    return (TW_SMEM ? sizeof(float4) * N : 0) +
+           sizeof(float2) * (multipass ? static_cast<size_t>(RB) * sw_row_stride(N) : 0);
 }
 
 } // namespace ppfg

@@ -1,26 +1,36 @@
-// fused.cuh — K3: polyphase FIR + C-point FFT in one persistent kernel
-// (channelize_block(ppf_fir_optimized(x)), pipeline.hpp:125-127), with no HBM
-// round trip for the filtered block.
+// fused.cuh — K3: polyphase FIR + C-point FFT in one persistent,
+// warp-specialised kernel (channelize_block(ppf_fir_optimized(x)),
+// pipeline.hpp:125-127) with no HBM round trip for the filtered block.
 //
-// Per CTA (one per SM): a contiguous range of output spectra, split into G
-// groups (G > 1 only when C < 256*R so that every CTA still has 256 threads).
-// Per group:
-//   * TMA ring: P slots of one input spectrum each (N*8 bytes), filled by
-//     1-D bulk copies (cp.async.bulk, SASS UBLKCP) on per-slot mbarriers; one
-//     producer lane per group refills slots as soon as a batch has consumed
-//     them, so HBM reads keep flowing while the CTA runs its FFT passes.
-//   * FIR threads: thread j owns the R = 2^RLOG channels j + k*N/R. It keeps
-//     their T-spectrum windows and taps in registers, slides them down the
-//     time axis (each input read once from the ring), and for each output
-//     spectrum immediately runs the first RLOG radix-2 stages on its R values
-//     in registers (they pair exactly those channels: labels differing in the
-//     top bits), then writes them to the FFT tile at the swizzled slots.
-//   * FFT passes over the tile (B spectra per group per batch): the remaining
-//     L - RLOG stages in register passes of <= W bits through shared memory;
-//     the final pass stores natural-order bins straight to HBM, coalesced.
+// One CTA per SM owns a contiguous range of output spectra, split into G
+// groups (G > 1 only for small C, so the FIR role always has 256 threads).
+// Two roles run concurrently, handing tiles over through shared memory:
+//
+//  FIR role (warpgroups 0-1, setmaxnreg.inc): thread j of group g owns the
+//    R = 2^RLOG channels j + k*N/R. Input spectra arrive in a P-slot TMA ring
+//    (cp.async.bulk 1-D copies, SASS UBLKCP, one mbarrier per slot). Each
+//    thread keeps its channels' T-spectrum windows and taps in registers,
+//    slides them down the time axis (every input spectrum read once), and per
+//    output spectrum runs the first RLOG radix-2 stages on its R values in
+//    registers (they pair exactly those channels), then stores them to the
+//    FFT tile at swizzled slots. Lane 0 of each group is the TMA producer:
+//    once all FIR warps of the group have released ring slot q-D (per-slot
+//    "empty" mbarrier), it refills that slot with spectrum q-D+P, so HBM
+//    reads never wait for a batch boundary.
+//
+//  FFT role (warpgroups 2-3, setmaxnreg.dec): the remaining L-RLOG stages of
+//    each tile in register passes of <= W = 4 bits through shared memory
+//    (named barrier between passes, FFT warps only); the final pass stores
+//    natural-order bins straight to HBM with coalesced 8-byte stores.
+//
+//  Handoff: two tiles; named barriers FULL[t] (FIR arrives, FFT syncs) and
+//  EMPTY[t] (FFT arrives, FIR syncs), so the FIR of tile b+1 overlaps the FFT
+//  of tile b.
+//
 // EXACT = true accumulates the FIR in FP64 in the reference order (bit-exact
-// to ppf_fir_optimized); false accumulates in FP32 (same order, one FMA per
-// tap). The FFT is always the reference's exact radix-2 arithmetic.
+// to ppf_fir_optimized); false accumulates in FP32, re and im together in one
+// FFMA2 per tap. The FFT is always the reference's exact radix-2 arithmetic
+// (packed FFMA2/FMUL2/FADD2, bit-identical, common.cuh bfly2).
 #pragma once
 
 #include <type_traits>
@@ -29,28 +39,51 @@
 
 namespace ppfg {
 
-template <int L_, int T_, int RLOG_, bool EXACT_>
+constexpr int ilcm(int a, int b) {
+    int x = a, y = b;
+    while (y) {
+        const int t = x % y;
+        x = y;
+        y = t;
+    }
+    return a / x * b;
+}
+
+template <int L_, int T_, int RLOG_, bool EXACT_, int FIR_REGS_ = 160, int FFT_REGS_ = 96>
 struct FusedCfg {
     static constexpr int L = L_, T = T_, RLOG = RLOG_;
     static constexpr bool EXACT = EXACT_;
+    static constexpr int FIR_REGS = FIR_REGS_, FFT_REGS = FFT_REGS_;
     static constexpr int N = 1 << L;
     static constexpr int R = 1 << RLOG;
-    static constexpr int NTG = N / R;                      // threads per group
-    static constexpr int NT = NTG >= 256 ? NTG : 256;      // threads per CTA
-    static constexpr int G = NT / NTG;                     // groups per CTA
-    static constexpr int B = 8;                            // output spectra per group per batch
-    static constexpr int P = 2 * B;                        // ring slots per group
-    static constexpr int W = 4;                            // FFT pass width (16 values/thread)
+    static constexpr int NTG = N / R;       // FIR threads per group
+    static constexpr int NFIR = 256;        // FIR role: warpgroups 0-1
+    static constexpr int NFFT = 256;        // FFT role: warpgroups 2-3
+    static constexpr int NT = NFIR + NFFT;
+    static constexpr int G = NFIR / NTG;    // groups per CTA
+    static constexpr int FW = NTG / 32;     // FIR warps per group
+    static constexpr int W = 4;             // FFT pass width: 16 values per unit
+    // spectra per group per batch (= per ring chunk and per tile): one FFT
+    // unit per FFT thread per pass
+    static constexpr int B = (NFFT << W) / (N * G) > 0 ? (NFFT << W) / (N * G) : 1;
+    static constexpr int PC = 4;            // ring chunks (of B input spectra) per group
+    // batches per unrolled FIR loop body, so the window rotation is pure renaming
+    static constexpr int BU = ilcm(B, T) / B;
     static constexpr unsigned STRIDE = sw_row_stride(N);
+    static constexpr size_t CHUNK_BYTES = sizeof(float2) * size_t(B) * N;
     // shared-memory layout (bytes)
-    static constexpr size_t TW_BYTES = sizeof(float2) * ((N + 1) & ~1);
+    static constexpr size_t TW_BYTES = sizeof(float4) * N;
     static constexpr size_t RING_OFF = (TW_BYTES + 127) & ~size_t(127);
-    static constexpr size_t RING_BYTES = sizeof(float2) * size_t(G) * P * N;
+    static constexpr size_t RING_BYTES = CHUNK_BYTES * G * PC;
     static constexpr size_t TILE_OFF = RING_OFF + RING_BYTES;
-    static constexpr size_t TILE_BYTES = sizeof(float2) * size_t(G) * B * STRIDE;
-    static constexpr size_t BAR_OFF = (TILE_OFF + TILE_BYTES + 7) & ~size_t(7);
-    static constexpr size_t SMEM = BAR_OFF + sizeof(uint64_t) * G * P;
-    static_assert(N % R == 0 && NT % NTG == 0, "bad fused shape");
+    static constexpr size_t TILE_ROWS = size_t(G) * B;
+    static constexpr size_t TILE_BYTES = sizeof(float2) * TILE_ROWS * STRIDE;
+    static constexpr size_t BAR_OFF = (TILE_OFF + 2 * TILE_BYTES + 7) & ~size_t(7);
+    static constexpr size_t SMEM = BAR_OFF + sizeof(uint64_t) * 2 * G * PC;
+    static_assert(NTG >= 32 && NTG <= NFIR && NFIR % NTG == 0, "FIR groups must be whole warps");
+    static_assert(FIR_REGS * NFIR + FFT_REGS * NFFT <= 65536, "register file");
+    static_assert(SMEM <= 232448, "shared memory per CTA");
+    static_assert(BU * B <= 32, "FIR unroll too large");
 };
 
 // Output-row map for the final FFT pass: tile row r = g*B + i is output
@@ -67,167 +100,185 @@ struct FusedRows {
     }
 };
 
+// named barriers: 0 = __syncthreads, FULL = 1+t, EMPTY = 3+t, FFT passes = 5
+PPFG_DEV void named_sync(int id, int count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+PPFG_DEV void named_arrive(int id, int count) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+struct SyncNamed {
+    int id, count;
+    PPFG_DEV void operator()() const { named_sync(id, count); }
+};
+
+PPFG_DEV void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 template <class Cfg>
 __global__ void __launch_bounds__(Cfg::NT, 1)
     fused_fir_fft_kernel(const float2* __restrict__ in, float2* __restrict__ out,
                          long long S_out, long long rows_per_cta, const float* __restrict__ taps,
-                         const float2* __restrict__ tw_g) {
+                         const float4* __restrict__ tw_g) {
     constexpr int L = Cfg::L, T = Cfg::T, RLOG = Cfg::RLOG, N = Cfg::N, R = Cfg::R;
-    constexpr int NTG = Cfg::NTG, NT = Cfg::NT, G = Cfg::G, B = Cfg::B, P = Cfg::P;
-    using Acc = typename std::conditional<Cfg::EXACT, double, float>::type;
+    constexpr int NTG = Cfg::NTG, NFIR = Cfg::NFIR, NFFT = Cfg::NFFT, NT = Cfg::NT;
+    constexpr int G = Cfg::G, B = Cfg::B;
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    float2* tw = reinterpret_cast<float2*>(smem_raw);
+    float4* tw = reinterpret_cast<float4*>(smem_raw);
     float2* ring = reinterpret_cast<float2*>(smem_raw + Cfg::RING_OFF);
-    float2* tile = reinterpret_cast<float2*>(smem_raw + Cfg::TILE_OFF);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + Cfg::BAR_OFF);
+    float2* tiles = reinterpret_cast<float2*>(smem_raw + Cfg::TILE_OFF);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + Cfg::BAR_OFF);
+    uint64_t* empty = full + G * Cfg::PC;
 
     const int tid = threadIdx.x;
-    const int g = tid / NTG;
-    const int j = tid - g * NTG;
-
     const long long o0 = static_cast<long long>(blockIdx.x) * rows_per_cta;
     const long long o1 = min(o0 + rows_per_cta, S_out);
     const long long rows_cta = max(o1 - o0, 0LL);
     const long long rpg = (rows_cta + G - 1) / G;
-    const long long og0 = o0 + g * rpg;
-    const long long og1 = min(og0 + rpg, o1);
-    const long long n_out_g = max(og1 - og0, 0LL);
-    const long long n_in_g = n_out_g > 0 ? n_out_g + T - 1 : 0;
-    const float2* gsrc = in + og0 * N; // input spectrum q of the group = og0 + q
-    float2* ring_g = ring + static_cast<size_t>(g) * P * N;
-    uint64_t* bars_g = bars + g * P;
+    const long long n_batches = (rpg + B - 1) / B;
 
     for (int i = tid; i < N - 1; i += NT)
         tw[i] = tw_g[i];
-    if (tid < G * P)
-        mbar_init(bars + tid, 1);
+    if (tid < G * Cfg::PC) {
+        mbar_init(full + tid, 1);
+        mbar_init(empty + tid, Cfg::FW);
+    }
     fence_mbar_init();
     __syncthreads();
 
-    // ---- producer (lane j == 0 of each group) ----
-    long long next_load = 0;
-    auto issue = [&](long long q) {
-        const int slot = static_cast<int>(q % P);
-        mbar_arrive_expect_tx(bars_g + slot, N * sizeof(float2));
-        bulk_g2s(ring_g + static_cast<size_t>(slot) * N, gsrc + q * N, N * sizeof(float2),
-                 bars_g + slot);
-    };
-    if (j == 0) {
-        for (; next_load < n_in_g && next_load < P; ++next_load)
-            issue(next_load);
+    if (tid >= NFIR) {
+        // ================================ FFT role ================================
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(Cfg::FFT_REGS));
+        const int ftid = tid - NFIR;
+        for (long long b = 0; b < n_batches; ++b) {
+            const int t = static_cast<int>(b & 1);
+            named_sync(1 + t, NT);
+            FftPasses<L, L - RLOG, Cfg::W, false, true, NFFT>::run(
+                nullptr, out, tiles + t * Cfg::TILE_ROWS * Cfg::STRIDE, Cfg::STRIDE,
+                static_cast<int>(Cfg::TILE_ROWS), FusedRows{o0, o1, rpg, b * B, B}, tw, ftid,
+                SyncNamed{5, NFFT});
+            named_arrive(3 + t, NT);
+        }
+        return;
     }
 
-    // ---- FIR state: taps and windows of channels c_k = j + k*NTG ----
+    // ================================== FIR role ==================================
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(Cfg::FIR_REGS));
+    using Acc = typename std::conditional<Cfg::EXACT, double, float>::type;
+    using Win = typename std::conditional<Cfg::EXACT, double2, float2>::type;
+    constexpr int PC = Cfg::PC, BU = Cfg::BU;
+    const int g = tid / NTG;
+    const int j = tid - g * NTG;
+    const bool producer = (j == 0);
+    const bool warp_leader = (tid & 31) == 0;
+    const long long og0 = o0 + g * rpg;
+    const long long og1 = min(og0 + rpg, o1);
+    const long long n_out_g = max(og1 - og0, 0LL);
+    const long long n_chunks = (n_out_g + B - 1) / B; // chunk c = outputs cB..cB+B-1
+    const float2* gsrc = in + og0 * N; // group input spectrum q = og0 + q
+    float2* ring_g = ring + static_cast<size_t>(g) * PC * B * N;
+    uint64_t* full_g = full + g * PC;
+    uint64_t* empty_g = empty + g * PC;
+
+    // chunk c = input spectra [T-1 + cB, T-1 + cB + B): the inputs batch c needs
+    auto issue = [&](long long c) {
+        const int slot = static_cast<int>(c % PC);
+        const long long rows = min(static_cast<long long>(B), n_out_g - c * B);
+        const uint32_t bytes = static_cast<uint32_t>(rows * N * sizeof(float2));
+        mbar_arrive_expect_tx(full_g + slot, bytes);
+        bulk_g2s(ring_g + static_cast<size_t>(slot) * B * N, gsrc + (T - 1 + c * B) * N, bytes,
+                 full_g + slot);
+    };
+    if (producer) {
+        for (long long c = 0; c < n_chunks && c < PC; ++c)
+            issue(c);
+    }
+
+    // taps and windows of channels c_k = j + k*NTG; window slots 1..T-1 hold
+    // the T-1 warm-up spectra (read straight from global: once per group)
     Acc h[R][T];
-    Acc xr[R][T], xi[R][T];
+    Win xw[R][T];
 #pragma unroll
     for (int k = 0; k < R; ++k) {
 #pragma unroll
         for (int t = 0; t < T; ++t) {
             h[k][t] = static_cast<Acc>(__ldg(taps + static_cast<size_t>(t) * N + j + k * NTG));
-            xr[k][t] = Acc(0);
-            xi[k][t] = Acc(0);
+            float2 x = make_float2(0.f, 0.f);
+            if (t >= 1 && n_out_g > 0)
+                x = __ldg(gsrc + static_cast<long long>(t - 1) * N + j + k * NTG);
+            xw[k][t].x = static_cast<Acc>(x.x);
+            xw[k][t].y = static_cast<Acc>(x.y);
         }
     }
-    auto read_row = [&](long long q, float2 (&x)[R]) {
-        const int slot = static_cast<int>(q % P);
-        mbar_wait(bars_g + slot, static_cast<uint32_t>((q / P) & 1));
-        const float2* row = ring_g + static_cast<size_t>(slot) * N + j;
+    // pre-stage twiddles tw[0 .. R-2] are the same for every spectrum
+    float4 twr[R > 1 ? R - 1 : 1];
 #pragma unroll
-        for (int k = 0; k < R; ++k)
-            x[k] = row[k * NTG];
-    };
-    // warm-up: the first T-1 inputs fill window slots 1..T-1
-#pragma unroll
-    for (int q = 0; q + 1 < T; ++q) {
-        float2 x[R];
-        if (q < n_in_g) {
-            read_row(q, x);
-        } else {
-#pragma unroll
-            for (int k = 0; k < R; ++k)
-                x[k] = make_float2(0.f, 0.f);
-        }
-#pragma unroll
-        for (int k = 0; k < R; ++k) {
-            xr[k][q + 1] = static_cast<Acc>(x[k].x);
-            xi[k][q + 1] = static_cast<Acc>(x[k].y);
-        }
-    }
-    __syncthreads();
-    if (j == 0) {
-        fence_proxy_async();
-        for (; next_load < n_in_g && next_load < (T - 1) + P; ++next_load)
-            issue(next_load);
-    }
+    for (int i = 0; i + 1 < R; ++i)
+        twr[i] = tw[i];
 
-    const long long n_batches = (rpg + B - 1) / B;
     const unsigned swj = sw(static_cast<unsigned>(j));
-    for (long long b = 0; b < n_batches; ++b) {
-        // ---- FIR phase: B output spectra per group ----
+    for (long long b0 = 0; b0 < n_batches; b0 += BU) {
 #pragma unroll
-        for (int i = 0; i < B; ++i) {
-            const long long rel = b * B + i;
-            const bool valid = rel < n_out_g;
-            float2 x[R];
-            if (valid) {
-                read_row(rel + T - 1, x);
-            } else {
+        for (int u = 0; u < BU; ++u) {
+            const long long b = b0 + u;
+            if (b >= n_batches)
+                break;
+            const int t = static_cast<int>(b & 1);
+            const int slot = static_cast<int>(b % PC);
+            const bool have = b < n_chunks;
+            if (producer && b >= 1 && b - 1 + PC < n_chunks) {
+                // refill the slot batch b-1 released
+                mbar_wait(empty_g + (b - 1) % PC, static_cast<uint32_t>(((b - 1) / PC) & 1));
+                fence_proxy_async();
+                issue(b - 1 + PC);
+            }
+            if (b >= 2)
+                named_sync(3 + t, NT); // the FFT role has drained tile t
+            if (have)
+                mbar_wait(full_g + slot, static_cast<uint32_t>((b / PC) & 1));
+            const float2* chunk = ring_g + static_cast<size_t>(slot) * B * N + j;
+            float2* tile = tiles + t * Cfg::TILE_ROWS * Cfg::STRIDE + g * B * Cfg::STRIDE + swj;
+#pragma unroll
+            for (int i = 0; i < B; ++i) {
+                const bool valid = b * B + i < n_out_g;
+                float2 y[R];
+#pragma unroll
+                for (int k = 0; k < R; ++k) {
+                    const float2 x = valid ? chunk[i * N + k * NTG] : make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int tt = 0; tt + 1 < T; ++tt)
+                        xw[k][tt] = xw[k][tt + 1];
+                    xw[k][T - 1].x = static_cast<Acc>(x.x);
+                    xw[k][T - 1].y = static_cast<Acc>(x.y);
+                    if constexpr (Cfg::EXACT) {
+                        double ar = __dmul_rn(h[k][0], xw[k][0].x);
+                        double ai = __dmul_rn(h[k][0], xw[k][0].y);
+#pragma unroll
+                        for (int tt = 1; tt < T; ++tt) {
+                            ar = __fma_rn(h[k][tt], xw[k][tt].x, ar);
+                            ai = __fma_rn(h[k][tt], xw[k][tt].y, ai);
+                        }
+                        y[k] = make_float2(__double2float_rn(ar), __double2float_rn(ai));
+                    } else {
+                        float2 acc = mul2s(h[k][0], xw[k][0]);
+#pragma unroll
+                        for (int tt = 1; tt < T; ++tt)
+                            acc = fma2s(h[k][tt], xw[k][tt], acc);
+                        y[k] = acc;
+                    }
+                }
+                fft_prestages<L, RLOG>(y, twr);
 #pragma unroll
                 for (int k = 0; k < R; ++k)
-                    x[k] = make_float2(0.f, 0.f);
+                    tile[i * Cfg::STRIDE + sw(static_cast<unsigned>(k * NTG))] = y[k];
             }
-            float2 y[R];
-#pragma unroll
-            for (int k = 0; k < R; ++k) {
-#pragma unroll
-                for (int t = 0; t + 1 < T; ++t) {
-                    xr[k][t] = xr[k][t + 1];
-                    xi[k][t] = xi[k][t + 1];
-                }
-                xr[k][T - 1] = static_cast<Acc>(x[k].x);
-                xi[k][T - 1] = static_cast<Acc>(x[k].y);
-                Acc ar, ai;
-                if constexpr (Cfg::EXACT) {
-                    ar = __dmul_rn(h[k][0], xr[k][0]);
-                    ai = __dmul_rn(h[k][0], xi[k][0]);
-#pragma unroll
-                    for (int t = 1; t < T; ++t) {
-                        ar = __fma_rn(h[k][t], xr[k][t], ar);
-                        ai = __fma_rn(h[k][t], xi[k][t], ai);
-                    }
-                    y[k] = make_float2(__double2float_rn(ar), __double2float_rn(ai));
-                } else {
-                    ar = __fmul_rn(h[k][0], xr[k][0]);
-                    ai = __fmul_rn(h[k][0], xi[k][0]);
-#pragma unroll
-                    for (int t = 1; t < T; ++t) {
-                        ar = __fmaf_rn(h[k][t], xr[k][t], ar);
-                        ai = __fmaf_rn(h[k][t], xi[k][t], ai);
-                    }
-                    y[k] = make_float2(ar, ai);
-                }
-            }
-            if constexpr (RLOG > 0)
-                fft_stages<L, L - RLOG, RLOG, true>(y, static_cast<unsigned>(j), tw);
-            float2* dst = tile + (g * B + i) * Cfg::STRIDE + swj;
-#pragma unroll
-            for (int k = 0; k < R; ++k)
-                dst[sw(static_cast<unsigned>(k * NTG))] = y[k];
+            __syncwarp();
+            if (have && warp_leader)
+                mbar_arrive(empty_g + slot); // this warp is done with the chunk
+            named_arrive(1 + t, NT);         // tile t is full
         }
-        __syncthreads();
-        // ---- refill the ring slots this batch consumed ----
-        if (j == 0) {
-            fence_proxy_async();
-            const long long consumed = (b + 1) * B + T - 1; // inputs 0..consumed-1 read
-            for (; next_load < n_in_g && next_load < consumed + P; ++next_load)
-                issue(next_load);
-        }
-        // ---- remaining FFT stages, final pass stores to HBM ----
-        FftPasses<L, L - RLOG, Cfg::W, false, true, NT>::run(
-            nullptr, out, tile, Cfg::STRIDE, G * B, FusedRows{o0, o1, rpg, b * B, B}, tw);
-        __syncthreads();
     }
 }
 

@@ -104,8 +104,11 @@ FusedEntry fused_entry() {
 // 6T fp64) for the FIR windows + taps, plus the FFT pass registers.
 const std::vector<FusedEntry>& fused_table() {
     static const std::vector<FusedEntry> t = {
-        fused_entry<FusedCfg<9, 8, 2, false>>(),
         fused_entry<FusedCfg<10, 8, 2, false>>(),
+        fused_entry<FusedCfg<9, 8, 2, false>>(),
+        fused_entry<FusedCfg<8, 8, 2, false>>(),
+        fused_entry<FusedCfg<7, 8, 2, false>>(),
+        fused_entry<FusedCfg<10, 4, 2, false>>(),
         fused_entry<FusedCfg<9, 8, 1, true>>(),
     };
     return t;
@@ -182,7 +185,7 @@ struct ppfg_plan_s {
     int L = -1; // log2 C when C is a power of two
     int num_sms = 148;
     float* d_taps = nullptr;     // [T][C] f32
-    float2* d_tw = nullptr;      // FftPlan twiddles, C-1 entries
+    float4* d_tw = nullptr;      // FftPlan twiddles (wr, wi, -wi, wr), C-1 entries
     double2* d_roots = nullptr;  // dft_naive roots, C entries (non-pow2)
     cudaStream_t stream = nullptr;
     bool own_stream = false;
@@ -200,15 +203,17 @@ struct ppfg_plan_s {
 
 namespace {
 
-// FftPlan twiddles exactly as dft.hpp:88-98: double angle -> cos/sin -> f32.
-std::vector<float2> host_twiddles(uint64_t n) {
-    std::vector<float2> tw(n > 1 ? n - 1 : 1);
+// FftPlan twiddles exactly as dft.hpp:88-98: double angle -> cos/sin -> f32,
+// stored as (wr, wi, -wi, wr) for the packed butterfly (common.cuh bfly2).
+std::vector<float4> host_twiddles(uint64_t n) {
+    std::vector<float4> tw(n > 1 ? n - 1 : 1);
     for (uint64_t len = 2; len <= n; len <<= 1) {
         const uint64_t half = len / 2;
         for (uint64_t j = 0; j < half; ++j) {
             const double angle = -2.0 * M_PI * static_cast<double>(j) / static_cast<double>(len);
-            tw[half - 1 + j] = make_float2(static_cast<float>(std::cos(angle)),
-                                           static_cast<float>(std::sin(angle)));
+            const float wr = static_cast<float>(std::cos(angle));
+            const float wi = static_cast<float>(std::sin(angle));
+            tw[half - 1 + j] = make_float4(wr, wi, -wi, wr);
         }
     }
     return tw;
@@ -271,7 +276,7 @@ __global__ void fft_bitrev_kernel(const float2* in, float2* out, int L, long lon
     out[g] = in[row * N + (__brev(p) >> (32 - L))];
 }
 
-__global__ void fft_stage_kernel(float2* data, const float2* __restrict__ tw, int L, int s,
+__global__ void fft_stage_kernel(float2* data, const float4* __restrict__ tw, int L, int s,
                                  long long n_rows) {
     const long long g = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     const long long half = 1LL << (s - 1);
@@ -284,7 +289,7 @@ __global__ void fft_stage_kernel(float2* data, const float2* __restrict__ tw, in
     const long long base = (q >> (s - 1)) << s;
     float2* r = data + (row << L);
     float2 lo = r[base + j], hi = r[base + j + half];
-    bfly(lo, hi, tw[half - 1 + j]);
+    bfly2(lo, hi, tw[half - 1 + j]);
     r[base + j] = lo;
     r[base + j + half] = hi;
 }
@@ -626,8 +631,8 @@ int ppfg_plan_create(ppfg_plan* plan, uint64_t n_channels, uint64_t n_taps,
     }
     if (p->L >= 1) {
         const auto tw = host_twiddles(n_channels);
-        if (cudaMalloc(&p->d_tw, tw.size() * sizeof(float2)) != cudaSuccess ||
-            cudaMemcpy(p->d_tw, tw.data(), tw.size() * sizeof(float2), cudaMemcpyHostToDevice) !=
+        if (cudaMalloc(&p->d_tw, tw.size() * sizeof(float4)) != cudaSuccess ||
+            cudaMemcpy(p->d_tw, tw.data(), tw.size() * sizeof(float4), cudaMemcpyHostToDevice) !=
                 cudaSuccess)
             return cleanup(fail(PPFG_CUDA_ERROR, "ppfg_plan_create: twiddle upload failed"));
     } else if (p->L < 0) {

@@ -152,7 +152,10 @@ class _Buf:
             self.n = n
             if x.is_cuda:
                 self.mem = MEM_DEVICE
-                self.stream = torch.cuda.current_stream(x.device).cuda_stream
+                # torch's default stream is the legacy stream (handle 0); the C-ABI
+                # reads NULL as "the plan's own stream", so name it explicitly
+                # (cudaStreamLegacy == 0x1).
+                self.stream = torch.cuda.current_stream(x.device).cuda_stream or 1
                 self.device = x.device.index
             else:
                 self.mem = MEM_HOST
