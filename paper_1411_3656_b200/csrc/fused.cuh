@@ -137,7 +137,9 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
     const long long o1 = min(o0 + rows_per_cta, S_out);
     const long long rows_cta = max(o1 - o0, 0LL);
     const long long rpg = (rows_cta + G - 1) / G;
-    const long long n_batches = (rpg + B - 1) / B;
+    // rounded up to whole FIR unrolls (BU batches): trailing batches are all
+    // padding rows, computed and never stored, so the FIR body has no exits
+    const long long n_batches = ((rpg + B - 1) / B + Cfg::BU - 1) / Cfg::BU * Cfg::BU;
 
     for (int i = tid; i < N - 1; i += NT)
         tw[i] = tw_g[i];
@@ -223,8 +225,6 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
 #pragma unroll
         for (int u = 0; u < BU; ++u) {
             const long long b = b0 + u;
-            if (b >= n_batches)
-                break;
             const int t = static_cast<int>(b & 1);
             const int slot = static_cast<int>(b % PC);
             const bool have = b < n_chunks;
@@ -240,13 +240,15 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
                 mbar_wait(full_g + slot, static_cast<uint32_t>((b / PC) & 1));
             const float2* chunk = ring_g + static_cast<size_t>(slot) * B * N + j;
             float2* tile = tiles + t * Cfg::TILE_ROWS * Cfg::STRIDE + g * B * Cfg::STRIDE + swj;
+            // Rows past the group's end (partial or absent chunk) read stale
+            // ring data: they only feed outputs the FFT role never stores, and
+            // keeping the loads unpredicated lets the window rotate by renaming.
 #pragma unroll
             for (int i = 0; i < B; ++i) {
-                const bool valid = b * B + i < n_out_g;
                 float2 y[R];
 #pragma unroll
                 for (int k = 0; k < R; ++k) {
-                    const float2 x = valid ? chunk[i * N + k * NTG] : make_float2(0.f, 0.f);
+                    const float2 x = chunk[i * N + k * NTG];
 #pragma unroll
                     for (int tt = 0; tt + 1 < T; ++tt)
                         xw[k][tt] = xw[k][tt + 1];

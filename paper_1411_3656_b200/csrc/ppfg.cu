@@ -108,6 +108,7 @@ const std::vector<FusedEntry>& fused_table() {
         fused_entry<FusedCfg<9, 8, 2, false>>(),
         fused_entry<FusedCfg<8, 8, 2, false>>(),
         fused_entry<FusedCfg<7, 8, 2, false>>(),
+        fused_entry<FusedCfg<6, 8, 1, false>>(),
         fused_entry<FusedCfg<10, 4, 2, false>>(),
         fused_entry<FusedCfg<9, 8, 1, true>>(),
     };
@@ -144,18 +145,34 @@ const FftEntry* fft_table(int L) {
     return &t[L];
 }
 
-KernelFn fir_table(int T) {
+struct FirEntry {
+    KernelFn fn;
+    int tc, k; // taps per lane, lanes per channel (T = tc * k)
+};
+
+template <int TC, int K>
+FirEntry fir_entry() {
+    constexpr int LAG = K == 1 ? 1 : (TC % 4 == 0 ? 4 : (TC % 2 == 0 ? 2 : 1));
+    return {reinterpret_cast<KernelFn>(&fir_chain_kernel<TC, K, LAG>), TC, K};
+}
+
+// K1 variants: one lane per channel up to T = 16; larger T split over K
+// lanes of up to 16 taps (T = TC * K), chained with a lag (fir.cuh).
+FirEntry fir_table(int T) {
     switch (T) {
-#define PPFG_FIR_CASE(t)                                                                          \
+#define PPFG_FIR(t, tc, k)                                                                        \
     case t:                                                                                       \
-        return reinterpret_cast<KernelFn>(&fir_exact_kernel<t>);
-        PPFG_FIR_CASE(1) PPFG_FIR_CASE(2) PPFG_FIR_CASE(3) PPFG_FIR_CASE(4) PPFG_FIR_CASE(5)
-        PPFG_FIR_CASE(6) PPFG_FIR_CASE(7) PPFG_FIR_CASE(8) PPFG_FIR_CASE(9) PPFG_FIR_CASE(10)
-        PPFG_FIR_CASE(11) PPFG_FIR_CASE(12) PPFG_FIR_CASE(13) PPFG_FIR_CASE(14)
-        PPFG_FIR_CASE(15) PPFG_FIR_CASE(16)
-#undef PPFG_FIR_CASE
+        return fir_entry<tc, k>();
+        PPFG_FIR(1, 1, 1) PPFG_FIR(2, 2, 1) PPFG_FIR(3, 3, 1) PPFG_FIR(4, 4, 1)
+        PPFG_FIR(5, 5, 1) PPFG_FIR(6, 6, 1) PPFG_FIR(7, 7, 1) PPFG_FIR(8, 8, 1)
+        PPFG_FIR(9, 9, 1) PPFG_FIR(10, 10, 1) PPFG_FIR(11, 11, 1) PPFG_FIR(12, 12, 1)
+        PPFG_FIR(13, 13, 1) PPFG_FIR(14, 14, 1) PPFG_FIR(15, 15, 1) PPFG_FIR(16, 16, 1)
+        PPFG_FIR(20, 10, 2) PPFG_FIR(24, 12, 2) PPFG_FIR(28, 14, 2) PPFG_FIR(32, 16, 2)
+        PPFG_FIR(40, 10, 4) PPFG_FIR(48, 16, 3) PPFG_FIR(56, 14, 4) PPFG_FIR(64, 16, 4)
+        PPFG_FIR(96, 16, 6) PPFG_FIR(128, 16, 8)
+#undef PPFG_FIR
     default:
-        return nullptr;
+        return {nullptr, 0, 0};
     }
 }
 
@@ -239,30 +256,35 @@ int launch_fir(ppfg_plan p, const float2* din, uint64_t S_in, float2* dout, cuda
                bool reference_order) {
     const uint64_t T = p->T, C = p->C;
     const uint64_t S_out = S_in - T + 1;
-    // segment length: >= 4T outputs so the (T-1) halo stays small; enough
-    // (channel, segment) work items to fill 148 SMs several times over.
-    const uint64_t target_threads = static_cast<uint64_t>(p->num_sms) * 2048 * 2;
-    uint64_t seg = cdiv(S_out * C, target_threads);
-    seg = std::max<uint64_t>(seg, std::min<uint64_t>(4 * T, S_out));
-    seg = std::max<uint64_t>(seg, 1);
-    const uint64_t n_seg = cdiv(S_out, seg);
-    const uint64_t n_work = n_seg * C;
-    const unsigned blocks = static_cast<unsigned>(cdiv(n_work, 256));
     const double init = reference_order ? 0.0 : -0.0;
-    KernelFn fn = fir_table(static_cast<int>(T));
-    long long S_out_ll = static_cast<long long>(S_out), n_work_ll = static_cast<long long>(n_work);
+    long long S_in_ll = static_cast<long long>(S_in), S_out_ll = static_cast<long long>(S_out);
     unsigned Cu = static_cast<unsigned>(C);
-    int seg_i = static_cast<int>(seg);
-    if (fn) {
-        void* args[] = {&din, &dout, &Cu, &S_out_ll, &p->d_taps, &seg_i, &n_work_ll,
+    const FirEntry e = fir_table(static_cast<int>(T));
+    if (e.fn) {
+        // warp tasks = (channel block of 32/K channels) x (time segment); segments
+        // long enough that the (TC-1) prefill and (K-1) pipeline drain stay small,
+        // and enough tasks to keep ~4 waves of 48 warps per SM busy.
+        const uint64_t cpw = 32 / e.k;
+        const uint64_t n_cb = cdiv(C, cpw);
+        const uint64_t target_tasks = static_cast<uint64_t>(p->num_sms) * 48 * 4;
+        uint64_t seg = cdiv(S_out * n_cb, target_tasks);
+        seg = std::max<uint64_t>(seg, std::min<uint64_t>(64, S_out));
+        const uint64_t n_seg = cdiv(S_out, seg);
+        long long n_tasks = static_cast<long long>(n_seg * n_cb);
+        int seg_i = static_cast<int>(seg);
+        const unsigned blocks = static_cast<unsigned>(cdiv(static_cast<uint64_t>(n_tasks) * 32, 256));
+        void* args[] = {&din, &dout, &Cu, &S_in_ll, &S_out_ll, &p->d_taps, &seg_i, &n_tasks,
                         const_cast<double*>(&init)};
-        PPFG_CUDA(cudaLaunchKernel(fn, dim3(blocks), dim3(256), args, 0, st));
-    } else {
-        fir_exact_generic_kernel<<<blocks, 256, 0, st>>>(din, dout, Cu, static_cast<unsigned>(T),
-                                                          S_out_ll, p->d_taps, seg_i, n_work_ll,
-                                                          init);
+        PPFG_CUDA(cudaLaunchKernel(e.fn, dim3(blocks), dim3(256), args, 0, st));
+        return check_launch("fir kernel");
     }
-    return check_launch("fir kernel");
+    const uint64_t target_threads = static_cast<uint64_t>(p->num_sms) * 2048 * 2;
+    uint64_t seg = std::max<uint64_t>(cdiv(S_out * C, target_threads), 1);
+    const uint64_t n_work = cdiv(S_out, seg) * C;
+    fir_exact_generic_kernel<<<static_cast<unsigned>(cdiv(n_work, 256)), 256, 0, st>>>(
+        din, dout, Cu, static_cast<unsigned>(T), S_out_ll, p->d_taps, static_cast<int>(seg),
+        static_cast<long long>(n_work), init);
+    return check_launch("fir kernel (generic T)");
 }
 
 // bit-exact radix-2 for any power-of-two size via global memory (large N)

@@ -33,7 +33,7 @@ def test_fir_golden_bitwise(cuda, golden):
 
 
 @pytest.mark.parametrize("C", [1, 2, 3, 8, 64, 100, 256, 1024, 4096])
-@pytest.mark.parametrize("T", [1, 2, 4, 7, 8, 16, 17, 32, 64])
+@pytest.mark.parametrize("T", [1, 2, 4, 7, 8, 16, 17, 20, 24, 32, 48, 64, 128])
 def test_fir_bitwise_vs_oracle(cuda, port, C, T):
     ppf = ppf_mod()
     rng = np.random.default_rng(C * 1000 + T)
