@@ -83,7 +83,8 @@ typedef struct {
  * does) and, for non-power-of-two C, the dft_naive root table (dft.hpp:47-51).
  * coeff_values may be NULL when n_taps == 0 (an FFT-only plan for
  * channelize_block). Validation mirrors check_fir_preconditions
- * (fir.hpp:56-65): n_channels >= 1, coefficient count == C*T. */
+ * (fir.hpp:56-65): n_channels >= 1, coefficient count == C*T. device = -1
+ * selects the calling thread's current CUDA device. */
 int ppfg_plan_create(ppfg_plan* plan, uint64_t n_channels, uint64_t n_taps,
                      const double* coeff_values, uint32_t flags, int device);
 int ppfg_plan_destroy(ppfg_plan plan);
@@ -190,6 +191,15 @@ int ppfg_generate_prototype(uint64_t n_channels, uint64_t n_taps, double beta,
 /* ---- metrics (bench.hpp:25-36, fir.hpp:49-52, dft.hpp:28-35) ----------------- */
 uint64_t ppfg_flops_for_fir(uint64_t n_channels, uint64_t n_taps, uint64_t n_spectra_out);
 uint64_t ppfg_flops_for_dft(uint64_t n_channels, uint64_t n_spectra);
+
+/* ---- device memory (for callers without their own CUDA runtime) --------------- */
+/* device = -1: the calling thread's current device. ppfg_memcpy infers the
+ * direction from the pointers (unified addressing) and is synchronous. */
+int ppfg_device_alloc(void** ptr, uint64_t bytes, int device);
+int ppfg_device_free(void* ptr);
+int ppfg_memcpy(void* dst, const void* src, uint64_t bytes);
+/* Wait for everything enqueued on the plan's stream. */
+int ppfg_plan_synchronize(ppfg_plan plan);
 
 /* ---- diagnostics --------------------------------------------------------------- */
 const char* ppfg_last_error(void);

@@ -50,6 +50,10 @@ SIGNATURES = {
     "ppfg_generate_prototype": (C.c_int, [u64, u64, C.c_double, C.c_double, dp]),
     "ppfg_flops_for_fir": (u64, [u64, u64, u64]),
     "ppfg_flops_for_dft": (u64, [u64, u64]),
+    "ppfg_device_alloc": (C.c_int, [C.POINTER(vp), u64, C.c_int]),
+    "ppfg_device_free": (C.c_int, [vp]),
+    "ppfg_memcpy": (C.c_int, [vp, vp, u64]),
+    "ppfg_plan_synchronize": (C.c_int, [vp]),
     "ppfg_last_error": (C.c_char_p, []),
     "ppfg_last_error_offset": (u64, []),
     "ppfg_kernel_launches": (u64, []),

@@ -624,7 +624,9 @@ int ppfg_plan_create(ppfg_plan* plan, uint64_t n_channels, uint64_t n_taps,
         cudaGetLastError();
         return fail(PPFG_NO_DEVICE, "ppfg: no CUDA device");
     }
-    if (device < 0 || device >= ndev)
+    if (device < 0 && cudaGetDevice(&device) != cudaSuccess) // -1: the caller's current device
+        return fail(PPFG_NO_DEVICE, "ppfg: no current device");
+    if (device >= ndev)
         return fail(PPFG_NO_DEVICE, "ppfg: device index out of range");
     DeviceGuard dg(device);
     cudaDeviceProp prop{};
@@ -1175,6 +1177,41 @@ int ppfg_process_stream(ppfg_plan p, uint64_t block_spectra, int zero_prime, int
         *state = s->st;
     ppfg_stream_destroy(s);
     return rc;
+}
+
+} // extern "C"
+
+// ========================================================= device memory
+extern "C" {
+
+int ppfg_device_alloc(void** ptr, uint64_t bytes, int device) {
+    if (!ptr)
+        return fail(PPFG_CONFIG_ERROR, "device_alloc: null pointer");
+    *ptr = nullptr;
+    if (device < 0 && cudaGetDevice(&device) != cudaSuccess)
+        return fail(PPFG_NO_DEVICE, "ppfg: no current device");
+    DeviceGuard dg(device);
+    PPFG_CUDA(cudaMalloc(ptr, bytes ? bytes : 1));
+    return PPFG_OK;
+}
+
+int ppfg_device_free(void* ptr) {
+    if (ptr)
+        PPFG_CUDA(cudaFree(ptr));
+    return PPFG_OK;
+}
+
+int ppfg_memcpy(void* dst, const void* src, uint64_t bytes) {
+    if (bytes)
+        PPFG_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyDefault));
+    return PPFG_OK;
+}
+
+int ppfg_plan_synchronize(ppfg_plan p) {
+    PPFG_TRY(check_plan(p));
+    DeviceGuard dg(p->device);
+    PPFG_CUDA(cudaStreamSynchronize(p->stream));
+    return PPFG_OK;
 }
 
 } // extern "C"
