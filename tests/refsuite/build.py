@@ -39,15 +39,26 @@ def build(which=("gpu", "cpu"), suites=SUITES):
     common = ["g++", "-std=gnu++20", "-O2", "-pthread", "-include", "algorithm",
               "-I", os.path.join(HERE), "-I", json_dir(), "-w"]
     lib_dir = os.path.join(ROOT, "paper_1411_3656_b200")
+    deps = [os.path.join(HERE, "gtest", "gtest.h")] + [
+        os.path.join(dp, f) for d in ("include/ppf_gpu", "include/ppf_dropin/ppf", "include")
+        for dp in [os.path.join(ROOT, d)] for f in os.listdir(dp) if f.endswith((".h", ".hpp"))]
+
+    def fresh(out, src):
+        if not os.path.exists(out):
+            return False
+        t = os.path.getmtime(out)
+        return all(os.path.getmtime(p) <= t for p in deps + [src, os.path.join(REF_TESTS,
+                                                                               "testing_util.hpp")])
+
     for s in suites:
         src = os.path.join(REF_TESTS, s + ".cpp")
-        if "gpu" in which:
+        if "gpu" in which and not fresh(os.path.join(OUT, s + "_gpu"), src):
             cmd = common + ["-I", os.path.join(ROOT, "include", "ppf_dropin"), "-I",
                             os.path.join(ROOT, "include"), src, "-o", os.path.join(OUT, s + "_gpu"),
                             "-L", lib_dir, "-lppfg",
                             "-Wl,-rpath,$ORIGIN/../../../paper_1411_3656_b200"]
             subprocess.check_call(cmd)
-        if "cpu" in which:
+        if "cpu" in which and not fresh(os.path.join(OUT, s + "_cpu"), src):
             cmd = common + ["-march=native", "-I", REF_INC, src, "-o", os.path.join(OUT, s + "_cpu")]
             subprocess.check_call(cmd)
     return True
