@@ -57,11 +57,15 @@ typedef enum { PPFG_MEM_HOST = 0, PPFG_MEM_DEVICE = 1 } ppfg_mem;
  * bit-identical to ppf_fir_optimized / channelize_block. PPFG_FAST lets the
  * fused FIR+FFT kernel accumulate the FIR in FP32 (max|err|/RMS well inside the
  * north-star 1e-5*log2(C) bound; FIR-only calls stay exact). PPFG_UNFUSED
- * forces FIR -> HBM -> FFT even where a fused kernel exists (for comparison). */
+ * forces FIR -> HBM -> FFT even where a fused kernel exists (for comparison).
+ * PPFG_CLUSTER allows the thread-block-cluster fused kernels (C >= 2048,
+ * T >= 16, FP64 at C = 1024), which are correct but, in round-1
+ * measurements, slower than the unfused path, so not taken by default. */
 enum {
     PPFG_EXACT = 0u,
     PPFG_FAST = 1u,
-    PPFG_UNFUSED = 2u
+    PPFG_UNFUSED = 2u,
+    PPFG_CLUSTER = 4u
 };
 
 typedef struct ppfg_plan_s* ppfg_plan;
@@ -121,7 +125,8 @@ int ppfg_fir_fft(ppfg_plan plan, const void* in, uint64_t n_spectra_in, void* ou
                  void* cuda_stream);
 
 /* Which kernel ppfg_fir_fft will run for this plan: 0 = unfused FIR+FFT,
- * 1 = fused FP32-FIR, 2 = fused FP64 (bit-exact) FIR. */
+ * 1 = fused FP32-FIR, 2 = fused FP64 (bit-exact) FIR, 3 / 4 = the cluster
+ * versions of 1 / 2. */
 int ppfg_fir_fft_kind(ppfg_plan plan);
 
 /* ---- single-row helpers (dft.hpp:39-66, 160-169), host memory ------------- */

@@ -81,9 +81,11 @@ PPFG_DEV void fft_prestages(float2 (&v)[1 << RLOG], const float4 (&twr)[RLOG > 0
 template <int L, int W>
 struct FftSchedule {
     static constexpr int NP = L == 0 ? 1 : (L + W - 1) / W;
-    static constexpr int width(int i) { return L / NP + (i < L % NP ? 1 : 0); }
-    static constexpr int done(int i) { return i * (L / NP) + (i < L % NP ? i : L % NP); }
-    static constexpr int lo(int i) { return L - done(i + 1); }
+    __host__ __device__ static constexpr int width(int i) { return L / NP + (i < L % NP ? 1 : 0); }
+    __host__ __device__ static constexpr int done(int i) {
+        return i * (L / NP) + (i < L % NP ? i : L % NP);
+    }
+    __host__ __device__ static constexpr int lo(int i) { return L - done(i + 1); }
 };
 
 // One pass of the row engine over a tile of rows.
@@ -106,8 +108,12 @@ PPFG_DEV void fft_tile_pass(const float2* gin, float2* gout,
     for (int unit = tid; unit < units; unit += NT) {
         const int r = unit / U;
         const unsigned u = static_cast<unsigned>(unit % U);
+        // a pass ending at label bit 0 maps lanes to the TOP label bits (bit-
+        // reversed unit index): its outputs are then consecutive bins and its
+        // twiddle reads consecutive table entries, whether it stores to global
+        // (FINAL) or back to the tile for further (cross-CTA) stages.
         unsigned fixed;
-        if constexpr (FINAL)
+        if constexpr (LO == 0)
             fixed = (L - W > 0) ? (crev_rt(u, L - W) << W) : 0u;
         else if constexpr (FIRST_GLOBAL)
             fixed = u;
@@ -149,21 +155,25 @@ PPFG_DEV void fft_tile_pass(const float2* gin, float2* gout,
 // `tid` is the thread's index among the NT threads running the passes and
 // `sync` the barrier between passes (__syncthreads, or a named barrier when
 // only the FFT warps of a warp-specialised CTA take part).
-template <int L, int LREM, int W, bool FIRST_GLOBAL, bool TW_SMEM, int NT, int I = 0>
+// STORE_LAST = false keeps the last pass's results in the tile (swizzled, by
+// label) instead of storing bins to global — used when more stages follow
+// (the cluster kernel's cross-CTA stages).
+template <int L, int LREM, int W, bool FIRST_GLOBAL, bool TW_SMEM, int NT, int I = 0,
+          bool STORE_LAST = true>
 struct FftPasses {
     using S = FftSchedule<LREM, W>;
     static constexpr int WI = S::width(I);
     static constexpr int LO = S::lo(I);
-    static constexpr bool FINAL = (I == S::NP - 1);
+    static constexpr bool LAST = (I == S::NP - 1);
     template <class RowMap, class Sync>
     PPFG_DEV static void run(const float2* gin, float2* gout, float2* tile, unsigned row_stride,
                              int rows, const RowMap& map, const float4* tw, int tid,
                              const Sync& sync) {
-        fft_tile_pass<L, LO, WI, FIRST_GLOBAL && I == 0, FINAL, TW_SMEM, NT>(
+        fft_tile_pass<L, LO, WI, FIRST_GLOBAL && I == 0, LAST && STORE_LAST, TW_SMEM, NT>(
             gin, gout, tile, row_stride, rows, map, tw, tid);
-        if constexpr (!FINAL) {
+        if constexpr (!LAST) {
             sync();
-            FftPasses<L, LREM, W, FIRST_GLOBAL, TW_SMEM, NT, I + 1>::run(
+            FftPasses<L, LREM, W, FIRST_GLOBAL, TW_SMEM, NT, I + 1, STORE_LAST>::run(
                 gin, gout, tile, row_stride, rows, map, tw, tid, sync);
         }
     }

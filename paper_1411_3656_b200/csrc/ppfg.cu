@@ -20,6 +20,7 @@
 #include "fft.cuh"
 #include "fir.cuh"
 #include "fused.cuh"
+#include "fused_cluster.cuh"
 
 namespace {
 
@@ -92,12 +93,19 @@ struct FusedEntry {
     size_t smem;
     int nt;
     int rows_per_batch; // B * G
+    int q;              // CTAs per cluster (1: single-SM kernel)
 };
 
 template <class Cfg>
 FusedEntry fused_entry() {
-    return {Cfg::L, Cfg::T, Cfg::EXACT, reinterpret_cast<KernelFn>(&fused_fir_fft_kernel<Cfg>),
-            Cfg::SMEM, Cfg::NT, Cfg::B * Cfg::G};
+    return {Cfg::L,    Cfg::T,  Cfg::EXACT, reinterpret_cast<KernelFn>(&fused_fir_fft_kernel<Cfg>),
+            Cfg::SMEM, Cfg::NT, Cfg::B * Cfg::G, 1};
+}
+
+template <class Cfg>
+FusedEntry cluster_entry() {
+    return {Cfg::L,    Cfg::T,  Cfg::EXACT, reinterpret_cast<KernelFn>(&fused_cluster_kernel<Cfg>),
+            Cfg::SMEM, Cfg::NT, Cfg::B * Cfg::G, Cfg::Q};
 }
 
 // Which (C, T) get a fused kernel. Register budget per SM ~ C * (3T fp32 |
@@ -110,7 +118,16 @@ const std::vector<FusedEntry>& fused_table() {
         fused_entry<FusedCfg<7, 8, 2, false>>(),
         fused_entry<FusedCfg<6, 8, 1, false>>(),
         fused_entry<FusedCfg<10, 4, 2, false>>(),
+        fused_entry<FusedCfg<9, 16, 1, false>>(),
         fused_entry<FusedCfg<9, 8, 1, true>>(),
+        // clusters (fused_cluster.cuh): C/Q channels per SM, DSMEM for the last log2 Q stages
+        cluster_entry<ClusterCfg<11, 1, 8, 2, false>>(),
+        cluster_entry<ClusterCfg<12, 2, 8, 2, false>>(),
+        cluster_entry<ClusterCfg<13, 3, 8, 2, false>>(),
+        cluster_entry<ClusterCfg<10, 1, 16, 1, false>>(),
+        cluster_entry<ClusterCfg<10, 2, 32, 0, false>>(),
+        cluster_entry<ClusterCfg<10, 1, 8, 1, true>>(),
+        cluster_entry<ClusterCfg<11, 2, 8, 1, true>>(),
     };
     return t;
 }
@@ -268,7 +285,7 @@ int launch_fir(ppfg_plan p, const float2* din, uint64_t S_in, float2* dout, cuda
         const uint64_t n_cb = cdiv(C, cpw);
         const uint64_t target_tasks = static_cast<uint64_t>(p->num_sms) * 48 * 4;
         uint64_t seg = cdiv(S_out * n_cb, target_tasks);
-        seg = std::max<uint64_t>(seg, std::min<uint64_t>(64, S_out));
+        seg = std::max<uint64_t>(seg, std::min<uint64_t>(std::max<uint64_t>(32, 2 * T), S_out));
         const uint64_t n_seg = cdiv(S_out, seg);
         long long n_tasks = static_cast<long long>(n_seg * n_cb);
         int seg_i = static_cast<int>(seg);
@@ -389,6 +406,33 @@ int launch_fused(ppfg_plan p, const float2* din, uint64_t S_in, float2* dout, cu
     const FusedEntry* e = p->fused;
     PPFG_TRY(ensure_smem_attr(e->fn, e->smem, p->device));
     const uint64_t S_out = S_in - p->T + 1;
+    if (e->q > 1) {
+        // one cluster of q CTAs per q SMs, all clusters co-resident (persistent)
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = e->q;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.blockDim = dim3(e->nt);
+        cfg.dynamicSmemBytes = e->smem;
+        cfg.stream = st;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cfg.gridDim = dim3(p->num_sms / e->q * e->q);
+        int max_clusters = 0;
+        PPFG_CUDA(cudaOccupancyMaxActiveClusters(&max_clusters, e->fn, &cfg));
+        if (max_clusters < 1)
+            return fail(PPFG_CUDA_ERROR, "fused cluster kernel: no cluster fits an SM group");
+        const uint64_t n_clusters = std::max<uint64_t>(
+            1, std::min<uint64_t>(max_clusters, cdiv(S_out, e->rows_per_batch)));
+        cfg.gridDim = dim3(static_cast<unsigned>(n_clusters * e->q));
+        long long rows_per_cluster = static_cast<long long>(cdiv(S_out, n_clusters));
+        long long S_out_ll = static_cast<long long>(S_out);
+        void* args[] = {&din, &dout, &S_out_ll, &rows_per_cluster, &p->d_taps, &p->d_tw};
+        PPFG_CUDA(cudaLaunchKernelExC(&cfg, e->fn, args));
+        return check_launch("fused cluster fir+fft kernel");
+    }
     const uint64_t grid =
         std::max<uint64_t>(1, std::min<uint64_t>(p->num_sms, cdiv(S_out, e->rows_per_batch)));
     long long rows_per_cta = static_cast<long long>(cdiv(S_out, grid));
@@ -399,6 +443,10 @@ int launch_fused(ppfg_plan p, const float2* din, uint64_t S_in, float2* dout, cu
     return check_launch("fused fir+fft kernel");
 }
 
+// Unfused: K1 writes the filtered spectra into the output buffer, K2
+// transforms them in place. (Chunking this into L2-resident pieces was
+// measured slower: per-chunk waves and launches cost more than the DRAM
+// round trip saves.)
 int launch_fir_fft(ppfg_plan p, const float2* din, uint64_t S_in, float2* dout, cudaStream_t st) {
     if (p->fused && !(p->flags & PPFG_UNFUSED))
         return launch_fused(p, din, S_in, dout, st);
@@ -679,8 +727,13 @@ int ppfg_plan_create(ppfg_plan* plan, uint64_t n_channels, uint64_t n_taps,
     }
     if (n_taps > 0 && p->L >= 0) {
         const bool exact = !(flags & PPFG_FAST);
+        // Cluster kernels are taken only on request (PPFG_CLUSTER): round-1
+        // measurements have them slower than FIR -> HBM -> FFT for every shape
+        // they cover; single-SM fused kernels are always faster.
+        const bool want_cluster = (flags & PPFG_CLUSTER) != 0;
         for (const auto& e : fused_table()) {
-            if (e.L == p->L && e.T == static_cast<int>(n_taps) && e.exact == exact) {
+            if (e.L == p->L && e.T == static_cast<int>(n_taps) && e.exact == exact &&
+                (e.q == 1 || want_cluster)) {
                 p->fused = &e;
                 break;
             }
@@ -727,7 +780,7 @@ void* ppfg_plan_stream(ppfg_plan plan) { return plan ? plan->stream : nullptr; }
 int ppfg_fir_fft_kind(ppfg_plan p) {
     if (!p || !p->fused || (p->flags & PPFG_UNFUSED))
         return 0;
-    return p->fused->exact ? 2 : 1;
+    return (p->fused->exact ? 2 : 1) + (p->fused->q > 1 ? 2 : 0);
 }
 
 int ppfg_fir(ppfg_plan p, const void* in, uint64_t n_spectra_in, void* out, int mem,

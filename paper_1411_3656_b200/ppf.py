@@ -19,6 +19,7 @@ from . import _lib
 EXACT = 0
 FAST = 1
 UNFUSED = 2
+CLUSTER = 4
 MEM_HOST = 0
 MEM_DEVICE = 1
 

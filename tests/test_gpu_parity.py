@@ -151,9 +151,9 @@ def test_fused_golden_exact(cuda, golden):
         assert np.array_equal(bits(got), bits(golden[f"ff{i}_y"])), (C, T)
 
 
-@pytest.mark.parametrize("C,T", [(512, 8), (1024, 8), (64, 8), (256, 4), (2048, 8), (8192, 8),
+@pytest.mark.parametrize("C,T", [(512, 8), (1024, 8), (64, 8), (256, 4), (2048, 8), (8192, 8), (4096, 8), (1024, 32),
                                  (1024, 4), (1024, 16), (512, 16), (128, 8)])
-@pytest.mark.parametrize("flags", ["exact", "fast"])
+@pytest.mark.parametrize("flags", ["exact", "fast", "exact+cluster", "fast+cluster"])
 def test_fused_vs_oracle(cuda, port, C, T, flags):
     ppf = ppf_mod()
     rng = np.random.default_rng(C + T)
@@ -163,11 +163,13 @@ def test_fused_vs_oracle(cuda, port, C, T, flags):
     x = ppf.synth(C, S * C, seed=C * 31 + T)
     coeffs = port.generate_prototype(C, T, 9.0)
     want = port.fir_fft(x, C, T, coeffs).view(np.complex64)
-    with ppf.Plan(C, T, coeffs, flags=ppf.EXACT if flags == "exact" else ppf.FAST) as p:
+    f = (ppf.EXACT if flags.startswith("exact") else ppf.FAST) | \
+        (ppf.CLUSTER if flags.endswith("cluster") else 0)
+    with ppf.Plan(C, T, coeffs, flags=f) as p:
         got = p.fir_fft(x)
         kind = p.kind
     assert got.shape == (S - T + 1, C)
-    if flags == "exact" or kind == 0:
+    if flags.startswith("exact") or kind == 0:
         assert np.array_equal(bits(got), bits(want)), f"kind={kind}"
     else:
         err = max_err_over_rms(got, want)
