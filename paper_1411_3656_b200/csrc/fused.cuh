@@ -49,7 +49,8 @@ constexpr int ilcm(int a, int b) {
     return a / x * b;
 }
 
-template <int L_, int T_, int RLOG_, bool EXACT_, int FIR_REGS_ = 160, int FFT_REGS_ = 96>
+template <int L_, int T_, int RLOG_, bool EXACT_, int FIR_REGS_ = 160, int FFT_REGS_ = 96,
+          int PC_ = 4>
 struct FusedCfg {
     static constexpr int L = L_, T = T_, RLOG = RLOG_;
     static constexpr bool EXACT = EXACT_;
@@ -66,7 +67,7 @@ struct FusedCfg {
     // spectra per group per batch (= per ring chunk and per tile): one FFT
     // unit per FFT thread per pass
     static constexpr int B = (NFFT << W) / (N * G) > 0 ? (NFFT << W) / (N * G) : 1;
-    static constexpr int PC = 4;            // ring chunks (of B input spectra) per group
+    static constexpr int PC = PC_;          // ring chunks (of B input spectra) per group
     // batches per unrolled FIR loop body, so the window rotation is pure renaming
     static constexpr int BU = ilcm(B, T) / B;
     static constexpr unsigned STRIDE = sw_row_stride(N);

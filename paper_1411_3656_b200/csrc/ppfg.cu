@@ -120,6 +120,14 @@ const std::vector<FusedEntry>& fused_table() {
         fused_entry<FusedCfg<10, 4, 2, false>>(),
         fused_entry<FusedCfg<9, 16, 1, false>>(),
         fused_entry<FusedCfg<9, 8, 1, true>>(),
+        // T = 1 with unit taps: x*1 == x exactly, so these are bit-exact,
+        // TMA-fed, warp-specialised FFTs — channelize_block for 64 <= C <= 2048
+        fused_entry<FusedCfg<6, 1, 0, false>>(),
+        fused_entry<FusedCfg<7, 1, 0, false>>(),
+        fused_entry<FusedCfg<8, 1, 0, false>>(),
+        fused_entry<FusedCfg<9, 1, 1, false>>(),
+        fused_entry<FusedCfg<10, 1, 2, false>>(),
+        fused_entry<FusedCfg<11, 1, 3, false, 160, 96, 3>>(),
         // clusters (fused_cluster.cuh): C/Q channels per SM, DSMEM for the last log2 Q stages
         cluster_entry<ClusterCfg<11, 1, 8, 2, false>>(),
         cluster_entry<ClusterCfg<12, 2, 8, 2, false>>(),
@@ -221,6 +229,8 @@ struct ppfg_plan_s {
     float* d_taps = nullptr;     // [T][C] f32
     float4* d_tw = nullptr;      // FftPlan twiddles (wr, wi, -wi, wr), C-1 entries
     double2* d_roots = nullptr;  // dft_naive roots, C entries (non-pow2)
+    float* d_ones = nullptr;     // C unit taps: channelize through the T = 1 fused kernel
+    const FusedEntry* fft_fused = nullptr;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     const FusedEntry* fused = nullptr;
@@ -333,6 +343,46 @@ __global__ void fft_stage_kernel(float2* data, const float4* __restrict__ tw, in
     r[base + j + half] = hi;
 }
 
+int launch_fused_entry(ppfg_plan p, const FusedEntry* e, const float* taps, uint64_t T,
+                       const float2* din, uint64_t S_in, float2* dout, cudaStream_t st) {
+    PPFG_TRY(ensure_smem_attr(e->fn, e->smem, p->device));
+    const uint64_t S_out = S_in - T + 1;
+    long long S_out_ll = static_cast<long long>(S_out);
+    if (e->q > 1) {
+        // one cluster of q CTAs per q SMs, all clusters co-resident (persistent)
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = e->q;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.blockDim = dim3(e->nt);
+        cfg.dynamicSmemBytes = e->smem;
+        cfg.stream = st;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cfg.gridDim = dim3(p->num_sms / e->q * e->q);
+        int max_clusters = 0;
+        PPFG_CUDA(cudaOccupancyMaxActiveClusters(&max_clusters, e->fn, &cfg));
+        if (max_clusters < 1)
+            return fail(PPFG_CUDA_ERROR, "fused cluster kernel: no cluster fits an SM group");
+        const uint64_t n_clusters = std::max<uint64_t>(
+            1, std::min<uint64_t>(max_clusters, cdiv(S_out, e->rows_per_batch)));
+        cfg.gridDim = dim3(static_cast<unsigned>(n_clusters * e->q));
+        long long rows_per_cluster = static_cast<long long>(cdiv(S_out, n_clusters));
+        void* args[] = {&din, &dout, &S_out_ll, &rows_per_cluster, &taps, &p->d_tw};
+        PPFG_CUDA(cudaLaunchKernelExC(&cfg, e->fn, args));
+        return check_launch("fused cluster fir+fft kernel");
+    }
+    const uint64_t grid =
+        std::max<uint64_t>(1, std::min<uint64_t>(p->num_sms, cdiv(S_out, e->rows_per_batch)));
+    long long rows_per_cta = static_cast<long long>(cdiv(S_out, grid));
+    void* args[] = {&din, &dout, &S_out_ll, &rows_per_cta, &taps, &p->d_tw};
+    PPFG_CUDA(cudaLaunchKernel(e->fn, dim3(static_cast<unsigned>(grid)), dim3(e->nt), args,
+                               e->smem, st));
+    return check_launch("fused fir+fft kernel");
+}
+
 int launch_channelize(ppfg_plan p, const float2* din, uint64_t rows, float2* dout,
                       bool fft_fallback, cudaStream_t st) {
     if (rows == 0)
@@ -365,6 +415,9 @@ int launch_channelize(ppfg_plan p, const float2* din, uint64_t rows, float2* dou
         return rc;
     }
     const int L = p->L;
+    if (p->fft_fused) // T = 1 fused kernel with unit taps (in place is safe: row s is
+                      // written only after it was read, and nothing else reads it)
+        return launch_fused_entry(p, p->fft_fused, p->d_ones, 1, din, rows, dout, st);
     if (const FftEntry* e = fft_table(L)) {
         PPFG_TRY(ensure_smem_attr(e->fn, e->smem, p->device));
         const uint64_t tiles = cdiv(rows, static_cast<uint64_t>(e->rows_per_tile));
@@ -403,44 +456,7 @@ int launch_channelize(ppfg_plan p, const float2* din, uint64_t rows, float2* dou
 }
 
 int launch_fused(ppfg_plan p, const float2* din, uint64_t S_in, float2* dout, cudaStream_t st) {
-    const FusedEntry* e = p->fused;
-    PPFG_TRY(ensure_smem_attr(e->fn, e->smem, p->device));
-    const uint64_t S_out = S_in - p->T + 1;
-    if (e->q > 1) {
-        // one cluster of q CTAs per q SMs, all clusters co-resident (persistent)
-        cudaLaunchConfig_t cfg = {};
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = e->q;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        cfg.blockDim = dim3(e->nt);
-        cfg.dynamicSmemBytes = e->smem;
-        cfg.stream = st;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        cfg.gridDim = dim3(p->num_sms / e->q * e->q);
-        int max_clusters = 0;
-        PPFG_CUDA(cudaOccupancyMaxActiveClusters(&max_clusters, e->fn, &cfg));
-        if (max_clusters < 1)
-            return fail(PPFG_CUDA_ERROR, "fused cluster kernel: no cluster fits an SM group");
-        const uint64_t n_clusters = std::max<uint64_t>(
-            1, std::min<uint64_t>(max_clusters, cdiv(S_out, e->rows_per_batch)));
-        cfg.gridDim = dim3(static_cast<unsigned>(n_clusters * e->q));
-        long long rows_per_cluster = static_cast<long long>(cdiv(S_out, n_clusters));
-        long long S_out_ll = static_cast<long long>(S_out);
-        void* args[] = {&din, &dout, &S_out_ll, &rows_per_cluster, &p->d_taps, &p->d_tw};
-        PPFG_CUDA(cudaLaunchKernelExC(&cfg, e->fn, args));
-        return check_launch("fused cluster fir+fft kernel");
-    }
-    const uint64_t grid =
-        std::max<uint64_t>(1, std::min<uint64_t>(p->num_sms, cdiv(S_out, e->rows_per_batch)));
-    long long rows_per_cta = static_cast<long long>(cdiv(S_out, grid));
-    long long S_out_ll = static_cast<long long>(S_out);
-    void* args[] = {&din, &dout, &S_out_ll, &rows_per_cta, &p->d_taps, &p->d_tw};
-    PPFG_CUDA(cudaLaunchKernel(e->fn, dim3(static_cast<unsigned>(grid)), dim3(e->nt), args,
-                               e->smem, st));
-    return check_launch("fused fir+fft kernel");
+    return launch_fused_entry(p, p->fused, p->d_taps, p->T, din, S_in, dout, st);
 }
 
 // Unfused: K1 writes the filtered spectra into the output buffer, K2
@@ -714,6 +730,19 @@ int ppfg_plan_create(ppfg_plan* plan, uint64_t n_channels, uint64_t n_taps,
                        cudaMemcpyHostToDevice) != cudaSuccess)
             return cleanup(fail(PPFG_CUDA_ERROR, "ppfg_plan_create: root upload failed"));
     }
+    if (p->L >= 0) {
+        for (const auto& e : fused_table()) {
+            if (e.L == p->L && e.T == 1 && e.q == 1) {
+                std::vector<float> ones(n_channels, 1.0f);
+                if (cudaMalloc(&p->d_ones, n_channels * sizeof(float)) != cudaSuccess ||
+                    cudaMemcpy(p->d_ones, ones.data(), n_channels * sizeof(float),
+                               cudaMemcpyHostToDevice) != cudaSuccess)
+                    return cleanup(fail(PPFG_CUDA_ERROR, "ppfg_plan_create: unit taps failed"));
+                p->fft_fused = &e;
+                break;
+            }
+        }
+    }
     if (cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&p->s_d2h, cudaStreamNonBlocking) != cudaSuccess)
@@ -752,6 +781,7 @@ int ppfg_plan_destroy(ppfg_plan p) {
     cudaFree(p->d_taps);
     cudaFree(p->d_tw);
     cudaFree(p->d_roots);
+    cudaFree(p->d_ones);
     for (int i = 0; i < 2; ++i) {
         cudaFree(p->d_in[i]);
         cudaFree(p->d_out[i]);
