@@ -50,7 +50,7 @@ constexpr int ilcm(int a, int b) {
 }
 
 template <int L_, int T_, int RLOG_, bool EXACT_, int FIR_REGS_ = 160, int FFT_REGS_ = 96,
-          int PC_ = 4>
+          int PC_ = 4, int FFT_WG_ = 2>
 struct FusedCfg {
     static constexpr int L = L_, T = T_, RLOG = RLOG_;
     static constexpr bool EXACT = EXACT_;
@@ -59,7 +59,7 @@ struct FusedCfg {
     static constexpr int R = 1 << RLOG;
     static constexpr int NTG = N / R;       // FIR threads per group
     static constexpr int NFIR = 256;        // FIR role: warpgroups 0-1
-    static constexpr int NFFT = 256;        // FFT role: warpgroups 2-3
+    static constexpr int NFFT = 128 * FFT_WG_; // FFT role: warpgroups 2 ..
     static constexpr int NT = NFIR + NFFT;
     static constexpr int G = NFIR / NTG;    // groups per CTA
     static constexpr int FW = NTG / 32;     // FIR warps per group
@@ -82,7 +82,10 @@ struct FusedCfg {
     static constexpr size_t BAR_OFF = (TILE_OFF + 2 * TILE_BYTES + 7) & ~size_t(7);
     static constexpr size_t SMEM = BAR_OFF + sizeof(uint64_t) * 2 * G * PC;
     static_assert(NTG >= 32 && NTG <= NFIR && NFIR % NTG == 0, "FIR groups must be whole warps");
-    static_assert(FIR_REGS * NFIR + FFT_REGS * NFFT <= 65536, "register file");
+    // setmaxnreg moves registers within the CTA's launch allocation only: the
+    // split must fit (65536 / NT) rounded down to 8, or .inc waits forever
+    static constexpr int LAUNCH_REGS = (65536 / NT) & ~7;
+    static_assert(FIR_REGS * NFIR + FFT_REGS * NFFT <= LAUNCH_REGS * NT, "register split");
     static_assert(SMEM <= 232448, "shared memory per CTA");
     static_assert(BU * B <= 32, "FIR unroll too large");
 };

@@ -133,7 +133,8 @@ struct ClusterCfg {
     static_assert(LQ >= 1 && LQ <= 3, "cluster of 2..8 CTAs");
     static_assert(LL >= LQ, "N/Q must be >= Q");
     static_assert(NTG >= 32 && NTG <= NFIR && NFIR % NTG == 0, "FIR groups must be whole warps");
-    static_assert(FIR_REGS * NFIR + FFT_REGS * NFFT <= 65536, "register file");
+    static constexpr int LAUNCH_REGS = (65536 / NT) & ~7;
+    static_assert(FIR_REGS * NFIR + FFT_REGS * NFFT <= LAUNCH_REGS * NT, "register split");
     static_assert(SMEM <= 232448, "shared memory per CTA");
     static_assert((BU * B) % PD == 0, "prefetch slots must be compile-time in the FIR body");
     static_assert(PD <= T - 1 + B || true, "");

@@ -112,7 +112,7 @@ FusedEntry cluster_entry() {
 // 6T fp64) for the FIR windows + taps, plus the FFT pass registers.
 const std::vector<FusedEntry>& fused_table() {
     static const std::vector<FusedEntry> t = {
-        fused_entry<FusedCfg<10, 8, 2, false>>(),
+        fused_entry<FusedCfg<10, 8, 2, false, 120, 80, 2, 3>>(),
         fused_entry<FusedCfg<9, 8, 2, false>>(),
         fused_entry<FusedCfg<8, 8, 2, false>>(),
         fused_entry<FusedCfg<7, 8, 2, false>>(),
