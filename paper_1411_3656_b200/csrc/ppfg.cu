@@ -109,21 +109,24 @@ FusedEntry cluster_entry() {
 }
 
 // Which (C, T) get a fused kernel. Register budget per SM ~ C * (3T fp32 |
-// 6T fp64) for the FIR windows + taps, plus the FFT pass registers.
+// 6T fp64) for the FIR windows + taps, plus the FFT pass registers. Entries
+// with (120, 80, 2, 3) run three FFT warpgroups (640 threads): measured faster
+// where the FFT role is critical (C=1024/T=8, C=64, T=1 at C<=128), slower
+// elsewhere (round-1 sweep, profiles/round1/sweep.md).
 const std::vector<FusedEntry>& fused_table() {
     static const std::vector<FusedEntry> t = {
         fused_entry<FusedCfg<10, 8, 2, false, 120, 80, 2, 3>>(),
         fused_entry<FusedCfg<9, 8, 2, false>>(),
         fused_entry<FusedCfg<8, 8, 2, false>>(),
         fused_entry<FusedCfg<7, 8, 2, false>>(),
-        fused_entry<FusedCfg<6, 8, 1, false>>(),
+        fused_entry<FusedCfg<6, 8, 1, false, 120, 80, 2, 3>>(),
         fused_entry<FusedCfg<10, 4, 2, false>>(),
         fused_entry<FusedCfg<9, 16, 1, false>>(),
         fused_entry<FusedCfg<9, 8, 1, true>>(),
         // T = 1 with unit taps: x*1 == x exactly, so these are bit-exact,
         // TMA-fed, warp-specialised FFTs — channelize_block for 64 <= C <= 2048
-        fused_entry<FusedCfg<6, 1, 0, false>>(),
-        fused_entry<FusedCfg<7, 1, 0, false>>(),
+        fused_entry<FusedCfg<6, 1, 0, false, 120, 80, 2, 3>>(),
+        fused_entry<FusedCfg<7, 1, 0, false, 120, 80, 2, 3>>(),
         fused_entry<FusedCfg<8, 1, 0, false>>(),
         fused_entry<FusedCfg<9, 1, 1, false>>(),
         fused_entry<FusedCfg<10, 1, 2, false>>(),
