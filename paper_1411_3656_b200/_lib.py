@@ -72,14 +72,19 @@ def load(build_if_needed: bool = True):
     with _lock:
         if _lib is not None:
             return _lib
-        if build_if_needed and _build.stale():
-            _build.build()
-        if not os.path.exists(_build.SO):
-            raise OSError(f"libppfg.so not found at {_build.SO}; run __graft_entry__.build()")
-        lib = C.CDLL(_build.SO)
+        so = os.environ.get("PPFG_SO")  # A/B experiments with another build of the library
+        if so is None:
+            if build_if_needed and _build.stale():
+                _build.build()
+            so = _build.SO
+        if not os.path.exists(so):
+            raise OSError(f"libppfg.so not found at {so}; run __graft_entry__.build()")
+        lib = C.CDLL(so)
         for name, (res, args) in SIGNATURES.items():
             f = getattr(lib, name)
             f.restype = res
             f.argtypes = args
+        if hasattr(lib, "ppfg_debug_trace"):  # -DPPFG_TRACE debug builds only
+            lib.ppfg_debug_trace.argtypes = [vp]
         _lib = lib
         return lib

@@ -67,8 +67,11 @@ PPFG_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
     mbar_wait(bar, parity);
     asm volatile("fence.acq_rel.cluster;" ::: "memory");
 }
-PPFG_DEV void mbar_arrive_remote_release(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+// "I have read my inbox": the inbox values were consumed (stored to HBM)
+// before the named barrier that precedes this arrive, so no fence is needed; a
+// release arrive here would make thread 0 wait for all its HBM stores.
+PPFG_DEV void mbar_arrive_remote_relaxed(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
                  : "memory");
 }
 PPFG_DEV void st_cluster_f2(uint32_t addr, float2 v) {
@@ -101,6 +104,26 @@ PPFG_DEV void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+#ifdef PPFG_TRACE
+// debug builds only (-DPPFG_TRACE): %globaltimer stamps of CTA 0's phases,
+// read back with ppfg_debug_trace
+__device__ unsigned long long g_trace[2][8][64];
+PPFG_DEV unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define PPFG_TR(role, b, ev)                                                                      \
+    do {                                                                                          \
+        if (blockIdx.x == 0 && (b) < 64)                                                          \
+            g_trace[role][ev][b] = gtimer();                                                      \
+    } while (0)
+#else
+#define PPFG_TR(role, b, ev)                                                                      \
+    do {                                                                                          \
+    } while (0)
+#endif
+
 template <int L_, int LQ_, int T_, int RLOG_, bool EXACT_, int FIR_REGS_ = 160, int FFT_REGS_ = 96>
 struct ClusterCfg {
     static constexpr int L = L_, LQ = LQ_, T = T_, RLOG = RLOG_;
@@ -119,7 +142,9 @@ struct ClusterCfg {
     static constexpr int BU = ilcm(B, T) / B;
     static constexpr int PD = (R >= 4 || EXACT) ? 4 : 8; // register prefetch depth (spectra)
     static constexpr unsigned STRIDE = sw_row_stride(NL);
-    static constexpr size_t TW_BYTES = sizeof(float4) * NL;
+    // the whole table (cross stages too) when it fits, else the local part
+    static constexpr bool TW_ALL = sizeof(float4) * N <= 80 * 1024;
+    static constexpr size_t TW_BYTES = sizeof(float4) * (TW_ALL ? N : NL);
     static constexpr size_t TILE_OFF = (TW_BYTES + 127) & ~size_t(127);
     static constexpr size_t TILE_ROWS = size_t(G) * B;
     static constexpr size_t TILE_BYTES = sizeof(float2) * TILE_ROWS * STRIDE;
@@ -166,8 +191,9 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
     const long long rpg = (rows_cta + G - 1) / G;
     const long long n_batches = ((rpg + B - 1) / B + BU - 1) / BU * BU;
 
-    for (int i = tid; i < NL - 1; i += NT)
-        tw[i] = tw_g[i]; // the local stages use tw[0 .. NL-2] only
+    for (int i = tid; i < (Cfg::TW_ALL ? N : NL) - 1; i += NT)
+        tw[i] = tw_g[i]; // local stages use tw[0 .. NL-2]; cross stages the rest
+    const float4* tw_x = Cfg::TW_ALL ? tw : tw_g;
     if (tid < 2) {
         mbar_init(ready + tid, 1);  // own expect_tx arrive + the pushed bytes
         mbar_init(freed + tid, Q);  // one arrival per owner CTA
@@ -186,53 +212,23 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
         constexpr int UPT = static_cast<int>(Cfg::TILE_ROWS) * UPR / NFFT;
         static_assert(static_cast<int>(Cfg::TILE_ROWS) * UPR % NFFT == 0, "cross units");
         static_assert(W1 >= LQ, "the owner CTA is a compile-time function of the lane's value");
-        constexpr uint32_t PAYLOAD = sizeof(float2) * Cfg::TILE_ROWS * NL; // bytes pushed to each CTA
+        // bytes each CTA receives from the other Q-1 CTAs per tile (own values
+        // are written locally)
+        constexpr uint32_t PAYLOAD = sizeof(float2) * Cfg::TILE_ROWS * (NL / Q) * (Q - 1);
         const int ftid = tid - NFIR;
         const uint32_t inbox_addr = smem_u32(inbox);
         const uint32_t ready_addr = smem_u32(ready);
-        for (long long b = 0; b < n_batches; ++b) {
-            const int t = static_cast<int>(b & 1);
-            float2* tile = tiles + t * Cfg::TILE_ROWS * Cfg::STRIDE;
-            const FusedRows map{o0, o1, rpg, b * B, B};
-            if (ftid == 0)
-                mbar_arrive_expect_tx(ready + t, PAYLOAD);
-            named_sync(1 + t, NT);
-            // local pass 0 (label bits [W1, LL-RLOG)), back into the tile
-            fft_tile_pass<LL, S::lo(0), S::width(0), false, false, true, NFFT>(
-                nullptr, nullptr, tile, Cfg::STRIDE, static_cast<int>(Cfg::TILE_ROWS), map, tw,
-                ftid);
-            named_sync(5, NFFT);
-            if (b >= 2) // every owner has read its inbox t from batch b-2
-                mbar_wait(freed + t, static_cast<uint32_t>(((b >> 1) - 1) & 1));
-            // local pass 1 (label bits [0, W1)); each value goes to the inbox of the
-            // CTA owning its cross group (label low bits), via st.async completing
-            // bytes on that CTA's ready[t]
-            for (int unit = ftid; unit < static_cast<int>(Cfg::TILE_ROWS) * U1; unit += NFFT) {
-                const int r = unit / U1;
-                const unsigned u = static_cast<unsigned>(unit - r * U1);
-                const unsigned fixed = crev_rt(u, LL - W1) << W1;
-                float2 v[1 << W1];
-                const float2* src = tile + r * Cfg::STRIDE + sw(fixed);
-#pragma unroll
-                for (int k = 0; k < (1 << W1); ++k)
-                    v[k] = src[sw(static_cast<unsigned>(k))];
-                fft_stages<LL, 0, W1, true>(v, fixed, tw);
-                const uint32_t slot0 =
-                    inbox_addr + static_cast<uint32_t>(
-                                     ((t * Q + static_cast<int>(rank)) * Cfg::TILE_ROWS + r) *
-                                         Cfg::IN_STRIDE + sw(fixed >> LQ)) * sizeof(float2);
-#pragma unroll
-                for (int k = 0; k < (1 << W1); ++k) {
-                    const uint32_t dest = static_cast<uint32_t>(k & (Q - 1));
-                    const uint32_t a = slot0 + sw(static_cast<unsigned>(k) >> LQ) * sizeof(float2);
-                    st_async_f2(mapa(a, dest), v[k], mapa(ready_addr + t * 8, dest));
-                }
-            }
-            named_arrive(3 + t, NT); // tile t may be refilled by the FIR role
-            mbar_wait(ready + t, static_cast<uint32_t>((b >> 1) & 1));
-            // cross-CTA stages: unit u of row r -> local label m = rev(u) << LQ | rank,
-            // its Q values sit in this CTA's inbox t, one per source CTA
-            const float2* ib = inbox + t * Q * Cfg::TILE_ROWS * Cfg::IN_STRIDE;
+        // Software-pipelined: iteration b runs the local passes of tile b, then
+        // the cross stages of tile b-1, so the partner CTAs' pushes for b-1
+        // have a whole local-pass time to land before they are waited for.
+        auto cross = [&](long long bp) {
+            const int tp = static_cast<int>(bp & 1);
+            const FusedRows map{o0, o1, rpg, bp * B, B};
+            mbar_wait(ready + tp, static_cast<uint32_t>((bp >> 1) & 1));
+            // unit u of row r -> local label m = rev(u) << LQ | rank; its Q values
+            // sit in this CTA's inbox tp, one per source CTA
+            if (ftid == 0) PPFG_TR(1, bp, 6);
+            const float2* ib = inbox + tp * Q * Cfg::TILE_ROWS * Cfg::IN_STRIDE;
             float2 v[UPT][Q];
             unsigned mm[UPT];
 #pragma unroll
@@ -259,7 +255,7 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
                             continue;
                         const unsigned n = (m << LQ) | static_cast<unsigned>(r2);
                         const unsigned j = __brev(n >> (bb + 1)) >> (33 - s);
-                        bfly2(v[i][r2], v[i][r2 | (1 << bb)], __ldg(tw_g + (half - 1 + j)));
+                        bfly2(v[i][r2], v[i][r2 | (1 << bb)], tw_x[half - 1 + j]);
                     }
                 }
                 const int unit = ftid + i * NFFT;
@@ -274,12 +270,68 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
                 }
             }
             named_sync(5, NFFT);
-            if (ftid == 0) { // inbox t is read: its writers may push into it again
+            if (ftid == 0) { // inbox tp is read: its writers may push into it again
 #pragma unroll
                 for (int r2 = 0; r2 < Q; ++r2)
-                    mbar_arrive_remote_release(mapa(smem_u32(freed + t), r2));
+                    mbar_arrive_remote_relaxed(mapa(smem_u32(freed + tp), r2));
             }
+        };
+        for (long long b = 0; b < n_batches; ++b) {
+            const int t = static_cast<int>(b & 1);
+            float2* tile = tiles + t * Cfg::TILE_ROWS * Cfg::STRIDE;
+            const FusedRows map{o0, o1, rpg, b * B, B};
+            if (ftid == 0)
+                mbar_arrive_expect_tx(ready + t, PAYLOAD);
+            if (ftid == 0) PPFG_TR(1, b, 0);
+            named_sync(1 + t, NT);
+            if (ftid == 0) PPFG_TR(1, b, 1);
+            // local pass 0 (label bits [W1, LL-RLOG)), back into the tile
+            fft_tile_pass<LL, S::lo(0), S::width(0), false, false, true, NFFT>(
+                nullptr, nullptr, tile, Cfg::STRIDE, static_cast<int>(Cfg::TILE_ROWS), map, tw,
+                ftid);
+            named_sync(5, NFFT);
+            if (ftid == 0) PPFG_TR(1, b, 2);
+            if (b >= 2) // every owner has read its inbox t from batch b-2
+                mbar_wait(freed + t, static_cast<uint32_t>(((b >> 1) - 1) & 1));
+            if (ftid == 0) PPFG_TR(1, b, 3);
+            // local pass 1 (label bits [0, W1)); each value goes to the inbox of the
+            // CTA owning its cross group (label low bits): st.async completing bytes
+            // on that CTA's ready[t], or a plain store for this CTA's own group
+            for (int unit = ftid; unit < static_cast<int>(Cfg::TILE_ROWS) * U1; unit += NFFT) {
+                const int r = unit / U1;
+                const unsigned u = static_cast<unsigned>(unit - r * U1);
+                const unsigned fixed = crev_rt(u, LL - W1) << W1;
+                float2 v[1 << W1];
+                const float2* src = tile + r * Cfg::STRIDE + sw(fixed);
+#pragma unroll
+                for (int k = 0; k < (1 << W1); ++k)
+                    v[k] = src[sw(static_cast<unsigned>(k))];
+                fft_stages<LL, 0, W1, true>(v, fixed, tw);
+                const uint32_t slot0 =
+                    inbox_addr + static_cast<uint32_t>(
+                                     ((t * Q + static_cast<int>(rank)) * Cfg::TILE_ROWS + r) *
+                                         Cfg::IN_STRIDE + sw(fixed >> LQ)) * sizeof(float2);
+#pragma unroll
+                for (int k = 0; k < (1 << W1); ++k) {
+                    const uint32_t dest = static_cast<uint32_t>(k & (Q - 1));
+                    const uint32_t a = slot0 + sw(static_cast<unsigned>(k) >> LQ) * sizeof(float2);
+                    if (dest == rank)
+                        asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(v[k].x),
+                                     "f"(v[k].y)
+                                     : "memory");
+                    else
+                        st_async_f2(mapa(a, dest), v[k], mapa(ready_addr + t * 8, dest));
+                }
+            }
+            if (ftid == 0) PPFG_TR(1, b, 4);
+            named_arrive(3 + t, NT); // tile t may be refilled by the FIR role
+            named_sync(5, NFFT);     // own-group values visible to every FFT thread
+            if (b >= 1)
+                cross(b - 1);
+            if (ftid == 0) PPFG_TR(1, b, 5);
         }
+        if (n_batches >= 1)
+            cross(n_batches - 1);
     } else {
         // ================================ FIR role ================================
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(Cfg::FIR_REGS));
@@ -339,8 +391,10 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
             for (int uu = 0; uu < BU; ++uu) {
                 const long long b = b0 + uu;
                 const int t = static_cast<int>(b & 1);
+                if (tid == 0) PPFG_TR(0, b, 0);
                 if (b >= 2) // this CTA's FFT role has read tile t (batch b-2)
                     named_sync(3 + t, NT);
+                if (tid == 0) PPFG_TR(0, b, 1);
                 float2* tile = tiles + t * Cfg::TILE_ROWS * Cfg::STRIDE + g * B * Cfg::STRIDE + swj;
 #pragma unroll
                 for (int i = 0; i < B; ++i) {
@@ -382,6 +436,7 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
                     for (int k = 0; k < R; ++k)
                         tile[i * Cfg::STRIDE + sw(static_cast<unsigned>(k * NTG))] = y[k];
                 }
+                if (tid == 0) PPFG_TR(0, b, 2);
                 named_arrive(1 + t, NT);
             }
         }

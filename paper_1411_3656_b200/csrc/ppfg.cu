@@ -94,18 +94,19 @@ struct FusedEntry {
     int nt;
     int rows_per_batch; // B * G
     int q;              // CTAs per cluster (1: single-SM kernel)
+    bool preferred;     // cluster kernels: faster than FIR -> HBM -> FFT (measured)
 };
 
 template <class Cfg>
 FusedEntry fused_entry() {
     return {Cfg::L,    Cfg::T,  Cfg::EXACT, reinterpret_cast<KernelFn>(&fused_fir_fft_kernel<Cfg>),
-            Cfg::SMEM, Cfg::NT, Cfg::B * Cfg::G, 1};
+            Cfg::SMEM, Cfg::NT, Cfg::B * Cfg::G, 1, true};
 }
 
 template <class Cfg>
-FusedEntry cluster_entry() {
+FusedEntry cluster_entry(bool preferred) {
     return {Cfg::L,    Cfg::T,  Cfg::EXACT, reinterpret_cast<KernelFn>(&fused_cluster_kernel<Cfg>),
-            Cfg::SMEM, Cfg::NT, Cfg::B * Cfg::G, Cfg::Q};
+            Cfg::SMEM, Cfg::NT, Cfg::B * Cfg::G, Cfg::Q, preferred};
 }
 
 // Which (C, T) get a fused kernel. Register budget per SM ~ C * (3T fp32 |
@@ -132,13 +133,14 @@ const std::vector<FusedEntry>& fused_table() {
         fused_entry<FusedCfg<10, 1, 2, false>>(),
         fused_entry<FusedCfg<11, 1, 3, false, 160, 96, 3>>(),
         // clusters (fused_cluster.cuh): C/Q channels per SM, DSMEM for the last log2 Q stages
-        cluster_entry<ClusterCfg<11, 1, 8, 2, false>>(),
-        cluster_entry<ClusterCfg<12, 2, 8, 2, false>>(),
-        cluster_entry<ClusterCfg<13, 3, 8, 2, false>>(),
-        cluster_entry<ClusterCfg<10, 1, 16, 1, false>>(),
-        cluster_entry<ClusterCfg<10, 2, 32, 0, false>>(),
-        cluster_entry<ClusterCfg<10, 1, 8, 1, true>>(),
-        cluster_entry<ClusterCfg<11, 2, 8, 1, true>>(),
+        // (preferred = default where round-1 measurements beat FIR -> HBM -> FFT)
+        cluster_entry<ClusterCfg<11, 1, 8, 2, false>>(false),
+        cluster_entry<ClusterCfg<12, 2, 8, 2, false>>(false),
+        cluster_entry<ClusterCfg<13, 3, 8, 2, false>>(false),
+        cluster_entry<ClusterCfg<10, 1, 16, 1, false>>(true),
+        cluster_entry<ClusterCfg<10, 2, 32, 0, false>>(true),
+        cluster_entry<ClusterCfg<10, 1, 8, 1, true>>(false),
+        cluster_entry<ClusterCfg<11, 2, 8, 1, true>>(false),
     };
     return t;
 }
@@ -759,13 +761,12 @@ int ppfg_plan_create(ppfg_plan* plan, uint64_t n_channels, uint64_t n_taps,
     }
     if (n_taps > 0 && p->L >= 0) {
         const bool exact = !(flags & PPFG_FAST);
-        // Cluster kernels are taken only on request (PPFG_CLUSTER): round-1
-        // measurements have them slower than FIR -> HBM -> FFT for every shape
-        // they cover; single-SM fused kernels are always faster.
+        // Cluster kernels: by default only where measured faster than
+        // FIR -> HBM -> FFT; PPFG_CLUSTER forces them.
         const bool want_cluster = (flags & PPFG_CLUSTER) != 0;
         for (const auto& e : fused_table()) {
             if (e.L == p->L && e.T == static_cast<int>(n_taps) && e.exact == exact &&
-                (e.q == 1 || want_cluster)) {
+                (e.q == 1 || want_cluster || e.preferred)) {
                 p->fused = &e;
                 break;
             }
@@ -1301,3 +1302,10 @@ int ppfg_plan_synchronize(ppfg_plan p) {
 }
 
 } // extern "C"
+
+#ifdef PPFG_TRACE
+extern "C" int ppfg_debug_trace(unsigned long long* out) {
+    PPFG_CUDA(cudaMemcpyFromSymbol(out, ppfg::g_trace, sizeof(ppfg::g_trace)));
+    return PPFG_OK;
+}
+#endif

@@ -29,7 +29,8 @@ def main():
     x = torch.empty((S, C), dtype=torch.complex64, device=dev)
     ppf.synth(C, S * C, seed=3, out=x)
     y = torch.empty((S - T + 1, C), dtype=torch.complex64, device=dev)
-    flags = {"fast": ppf.FAST, "exact": ppf.EXACT, "unfused": ppf.UNFUSED}[a.mode]
+    flags = {"fast": ppf.FAST, "exact": ppf.EXACT, "unfused": ppf.UNFUSED,
+             "cluster": ppf.FAST | ppf.CLUSTER, "exact-cluster": ppf.CLUSTER}[a.mode]
     with ppf.Plan(C, T, ppf.generate_prototype(C, T), flags=flags) as p:
         for _ in range(a.reps):
             if a.op == "fir":
