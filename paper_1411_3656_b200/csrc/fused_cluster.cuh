@@ -107,7 +107,7 @@ PPFG_DEV void cp_async_wait() {
 #ifdef PPFG_TRACE
 // debug builds only (-DPPFG_TRACE): %globaltimer stamps of CTA 0's phases,
 // read back with ppfg_debug_trace
-__device__ unsigned long long g_trace[2][8][64];
+__device__ unsigned long long g_trace[2][16][64];
 PPFG_DEV unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

@@ -1,0 +1,408 @@
+// fused_split.cuh — K3s: the fused FIR+FFT for channel/tap counts whose FIR
+// state does not fit one SM's register file (C >= 2048, T >= 16, FP64 at
+// C = 1024), on a thread-block cluster of Q = 2^LQ CTAs (one per SM).
+//
+// The split is a transpose through distributed shared memory:
+//  - FIR role of CTA r filters channels k*N/R + r*256 + j (k < R, j < 256)
+//    of EVERY output spectrum of the cluster's range: each thread holds only
+//    R = N/(Q*256) channels' windows and taps; they are exactly the labels
+//    the first log2 R FFT stages pair, so the thread runs those stages in
+//    registers (as in fused.cuh); and the CTA's input is R contiguous runs of
+//    256 channels per spectrum, fetched by TMA bulk copies (cp.async.bulk,
+//    SASS UBLKCP) into a local ring.
+//  - FFT role of CTA d transforms the full C-point rows of batches
+//    b = d, d+Q, d+2Q, ... (B spectra each): the remaining L - log2 R stages
+//    in register passes of <= 5 label bits (fft.cuh; the swizzle is
+//    bank-conflict-free for these schedules), with no cross-CTA FFT stage.
+//  - The FIR writes batch b's outputs straight into its owner's tile: the
+//    owner's own channels with st.shared, the other CTAs' with st.async
+//    over DSMEM, whose bytes complete on the owner's full[t] mbarrier.
+//
+// Synchronisation per owner tile t (two tiles per CTA):
+//   local FIR block written  : named barrier FULL[t] (FIR arrives, FFT syncs)
+//   remote FIR blocks landed : full[t] mbarrier; the owner's FFT leader arms
+//                              it (arrive.expect_tx of the Q-1 remote blocks)
+//                              before it announces the tile free
+//   tile t of CTA d free     : empty[d][t] mbarrier in every CTA, one remote
+//                              arrive from d's FFT leader after its last read
+// A cluster barrier after mbarrier init and before exit keeps every CTA's
+// shared memory alive while others may still address it.
+#pragma once
+
+#include <cuda.h>
+
+#include "fused_cluster.cuh"
+
+namespace ppfg {
+
+// one predicated store, no branch: st.shared into this CTA's tile, or
+// st.async into the owner's tile with its bytes completing on the owner's
+// full[t] mbarrier. No "memory" clobber: the ring loads of later rows may be
+// scheduled above it (the tile is never read by this role; ordering against
+// the barrier operations, all volatile asm, is kept).
+PPFG_DEV void st_local_or_async_f2(bool local, uint32_t laddr, uint32_t raddr, float2 v,
+                                   uint32_t rbar) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.u32 p, %0, 0;\n\t"
+        "@p st.shared.v2.f32 [%1], {%3, %4};\n\t"
+        "@!p st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%2], {%3, %4}, [%5];\n\t}" ::"r"(
+            static_cast<uint32_t>(local)),
+        "r"(laddr), "r"(raddr), "f"(v.x), "f"(v.y), "r"(rbar));
+}
+
+// "this warp has read its ring slot": its reads completed when their values
+// were consumed, so no release semantics are needed — a release arrive would
+// first wait for this thread's outstanding DSMEM stores
+PPFG_DEV void mbar_arrive_relaxed(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// 3-D TMA tensor copy global -> this CTA's shared memory (SASS UTMALDG),
+// completing its bytes on a local mbarrier
+PPFG_DEV void tma_load_3d(void* smem_dst, const CUtensorMap* map, int c0, int c1, int c2,
+                          uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// move this warpgroup's register budget from the launch allocation to REGS
+template <int REGS, int LAUNCH>
+PPFG_DEV void set_max_regs() {
+    if constexpr (REGS > LAUNCH)
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(REGS));
+    else if constexpr (REGS < LAUNCH)
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(REGS));
+}
+
+template <int L_, int LQ_, int T_, bool EXACT_, int FIR_WG_ = 2, int W_ = 5,
+          int FIR_REGS_ = 152, int FFT_REGS_ = 104, int PC_ = 0>
+struct SplitCfg {
+    static constexpr int L = L_, LQ = LQ_, T = T_;
+    static constexpr bool EXACT = EXACT_;
+    static constexpr int FIR_REGS = FIR_REGS_, FFT_REGS = FFT_REGS_;
+    static constexpr int Q = 1 << LQ;
+    static constexpr int N = 1 << L;
+    static constexpr int NFIR = 128 * FIR_WG_, NFFT = 256, NT = NFIR + NFFT;
+    static constexpr int R = N / (Q * NFIR); // channels per FIR thread
+    static constexpr int RLOG = R == 1 ? 0 : R == 2 ? 1 : R == 4 ? 2 : 3;
+    static constexpr int LREM = L - RLOG;    // stages left to the FFT role
+    static constexpr int W = W_;
+    static constexpr int WMAX = FftSchedule<LREM, W>::width(0);
+    static constexpr int B = (NFFT << WMAX) / N > 0 ? (NFFT << WMAX) / N : 1; // spectra per batch
+    static constexpr int BU = ilcm(B, T) / B; // batches per unrolled FIR body (window renaming)
+    static constexpr int BQ = ilcm(BU, Q);    // n_batches granule: whole bodies, equal fills per CTA
+    static constexpr int RUN = NFIR;          // channels per contiguous input run
+    static constexpr unsigned STRIDE = sw_row_stride(N);
+    static constexpr size_t TILE_FLOATS2 = size_t(B) * STRIDE;
+    static constexpr size_t TILE_BYTES = sizeof(float2) * TILE_FLOATS2;
+    // input ring: one chunk = RB spectra x R runs x RUN channels, ONE TMA
+    // tensor copy (3-D box {RUN, R, RB} of 8-byte elements)
+    static constexpr size_t AVAIL = 232448 - 2 * TILE_BYTES - 512;
+    // twiddles in shared memory when that still leaves >= 48 KB of ring
+    static constexpr bool TW_SMEM = sizeof(float4) * N + 48 * 1024 <= AVAIL;
+    static constexpr size_t TW_BYTES = TW_SMEM ? sizeof(float4) * N : 0;
+    static constexpr size_t RING_MAX = (AVAIL - TW_BYTES) < 96 * 1024 ? (AVAIL - TW_BYTES) : 96 * 1024;
+    static constexpr size_t ROW_BYTES = sizeof(float2) * R * RUN; // one spectrum's runs
+    // rows per chunk: the whole batch if two such chunks fit, else halves...
+    static constexpr int RB = RING_MAX / (ROW_BYTES * B) >= 2 ? B
+                              : (B % 2 == 0 && RING_MAX / (ROW_BYTES * (B / 2)) >= 2) ? B / 2
+                                                                                        : 1;
+    static constexpr size_t CHUNK_FLOATS2 = size_t(RB) * R * RUN;
+    static constexpr size_t CHUNK_BYTES = sizeof(float2) * CHUNK_FLOATS2;
+    static constexpr int PC = PC_ > 0 ? PC_ : int(RING_MAX / CHUNK_BYTES) < 64 ? int(RING_MAX / CHUNK_BYTES) : 64;
+    static constexpr size_t RING_BYTES = CHUNK_BYTES * PC;
+    static constexpr size_t BARS = sizeof(uint64_t) * (2 * PC + 2 + 2 * Q);
+    static constexpr size_t RING_OFF = (TW_BYTES + 127) & ~size_t(127);
+    static constexpr size_t TILE_OFF = RING_OFF + RING_BYTES;
+    static constexpr size_t BAR_OFF = (TILE_OFF + 2 * TILE_BYTES + 7) & ~size_t(7);
+    // ring_full[PC], ring_empty[PC], full[2], empty[Q][2]
+    static constexpr size_t SMEM = BAR_OFF + BARS;
+    static constexpr uint32_t REMOTE_BYTES = uint32_t(sizeof(float2)) * (Q - 1) * B * (N / Q);
+    static_assert(Q >= 2 && Q <= 8, "portable cluster sizes");
+    static_assert(R >= 1 && R <= 8 && R * Q * NFIR == N, "every FIR thread owns whole channels");
+    static constexpr int LAUNCH_REGS = (65536 / NT) & ~7;
+    static_assert(FIR_REGS * NFIR + FFT_REGS * NFFT <= LAUNCH_REGS * NT, "register split");
+    static_assert(SMEM <= 232448, "shared memory per CTA");
+    static_assert(PC >= 2, "input ring too shallow");
+    static_assert(B % RB == 0, "whole chunks per batch");
+    static_assert(RUN <= 256 && R <= 256 && RB <= 256, "TMA box dimensions");
+    static_assert(BU * B <= 32, "FIR unroll too large");
+};
+
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::NT, 1)
+    fused_split_kernel(const __grid_constant__ CUtensorMap in_map, const float2* __restrict__ in,
+                       float2* __restrict__ out, long long S_out,
+                       long long rows_per_cluster, const float* __restrict__ taps,
+                       const float4* __restrict__ tw_g) {
+    constexpr int T = Cfg::T, N = Cfg::N, R = Cfg::R, RLOG = Cfg::RLOG, Q = Cfg::Q;
+    constexpr int NFIR = Cfg::NFIR, NFFT = Cfg::NFFT, NT = Cfg::NT, B = Cfg::B, PC = Cfg::PC;
+    constexpr int BU = Cfg::BU, RUN = Cfg::RUN;
+
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    float4* tw_s = reinterpret_cast<float4*>(smem_raw);
+    float2* ring = reinterpret_cast<float2*>(smem_raw + Cfg::RING_OFF);
+    float2* tiles = reinterpret_cast<float2*>(smem_raw + Cfg::TILE_OFF);
+    uint64_t* ring_full = reinterpret_cast<uint64_t*>(smem_raw + Cfg::BAR_OFF);
+    uint64_t* ring_empty = ring_full + PC;
+    uint64_t* full = ring_empty + PC;
+    uint64_t* empty = full + 2; // empty[d * 2 + t]
+
+    const int tid = threadIdx.x;
+    const uint32_t rank = cluster_rank();
+    const long long cid = blockIdx.x / Q;
+    const long long o0 = cid * rows_per_cluster;
+    const long long o1 = min(o0 + rows_per_cluster, S_out);
+    const long long rows = max(o1 - o0, 0LL);
+    // whole unrolled bodies and equal fills per CTA: trailing batches are
+    // padding rows, computed (from stale ring slots) and never stored
+    const long long n_batches = ((rows + B - 1) / B + Cfg::BQ - 1) / Cfg::BQ * Cfg::BQ;
+
+    if constexpr (Cfg::TW_SMEM) {
+        for (int i = tid; i < N - 1; i += NT)
+            tw_s[i] = tw_g[i];
+    }
+    if (tid < PC) {
+        mbar_init(ring_full + tid, 1);
+        mbar_init(ring_empty + tid, NFIR / 32);
+    } else if (tid < PC + 2) {
+        mbar_init(full + (tid - PC), 1);
+    } else if (tid < PC + 2 + 2 * Q) {
+        mbar_init(empty + (tid - PC - 2), 1);
+    }
+    fence_mbar_init();
+    __syncthreads();
+    if (tid == NFIR) { // arm both tiles for their first fill
+        mbar_arrive_expect_tx(full + 0, Cfg::REMOTE_BYTES);
+        mbar_arrive_expect_tx(full + 1, Cfg::REMOTE_BYTES);
+    }
+    cluster_sync_all(); // every CTA's barriers exist before anyone addresses them
+
+    if (tid >= NFIR) {
+        // ================================ FFT role ================================
+        set_max_regs<Cfg::FFT_REGS, Cfg::LAUNCH_REGS>();
+        const int ftid = tid - NFIR;
+        const float4* tw = Cfg::TW_SMEM ? tw_s : tw_g;
+        const long long n_fills = n_batches / Q;
+        for (long long f = 0; f < n_fills; ++f) {
+            const int t = static_cast<int>(f & 1);
+            const long long b = f * Q + rank;
+            float2* tile = tiles + t * Cfg::TILE_FLOATS2;
+            if (ftid == 0) PPFG_TR(1, f, 0);
+            named_sync(1 + t, NFIR + NFFT);                          // own block written
+            if (ftid == 0) PPFG_TR(1, f, 1);
+            mbar_wait(full + t, static_cast<uint32_t>((f >> 1) & 1)); // remote blocks landed
+            if (ftid == 0) PPFG_TR(1, f, 2);
+            FftPasses<Cfg::L, Cfg::LREM, Cfg::W, false, Cfg::TW_SMEM, NFFT>::run(
+                nullptr, out, tile, Cfg::STRIDE, B, FusedRows{o0, o1, rows, b * B, B}, tw, ftid,
+                SyncNamed{5, NFFT});
+            named_sync(5, NFFT); // every read of the tile has completed
+            if (ftid == 0) PPFG_TR(1, f, 3);
+            if (ftid == 0) {
+                mbar_arrive_expect_tx(full + t, Cfg::REMOTE_BYTES); // arm the next fill
+                const uint32_t e = smem_u32(empty + rank * 2 + t);
+#pragma unroll
+                for (int q = 0; q < Q; ++q)
+                    mbar_arrive_remote_relaxed(mapa(e, static_cast<uint32_t>(q)));
+            }
+        }
+        cluster_sync_all();
+        return;
+    }
+
+    // ================================== FIR role ==================================
+    set_max_regs<Cfg::FIR_REGS, Cfg::LAUNCH_REGS>();
+    using Acc = typename std::conditional<Cfg::EXACT, double, float>::type;
+    using Win = typename std::conditional<Cfg::EXACT, double2, float2>::type;
+    // thread j owns channels c_k = k*N/R + rank*RUN + j: the R labels the
+    // first RLOG stages pair, and R contiguous runs of RUN channels per CTA
+    const int j = tid;
+    const bool producer = (j == 0);
+    const bool warp_leader = (tid & 31) == 0;
+    const float2* gsrc = in + o0 * N + rank * RUN; // run 0 of input spectrum o0 + q
+
+    // chunk c = input spectra T-1 + c*RB .. +RB (their R runs of this CTA);
+    // rows past the input's end are zero-filled by TMA (they feed only
+    // padding outputs)
+    const long long n_chunks = (rows + Cfg::RB - 1) / Cfg::RB;
+    auto issue = [&](long long c, int slot) {
+        mbar_arrive_expect_tx(ring_full + slot, static_cast<uint32_t>(Cfg::CHUNK_BYTES));
+        tma_load_3d(ring + slot * Cfg::CHUNK_FLOATS2, &in_map, static_cast<int>(rank * RUN), 0,
+                    static_cast<int>(o0 + T - 1 + c * Cfg::RB), ring_full + slot);
+    };
+    if (producer) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&in_map)) : "memory");
+        for (long long c = 0; c < n_chunks && c < PC; ++c)
+            issue(c, static_cast<int>(c));
+    }
+    // ring cursors: consumer (chunk c) and refill, slot + parity
+    // (rc = next chunk to issue; it reuses the slot of chunk rc - PC)
+    int cslot = 0, rslot = 0;
+    uint32_t cphase = 0, rphase = 0;
+    long long rc = PC;
+
+    Acc h[R][T];
+    Win xw[R][T];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+#pragma unroll
+        for (int t = 0; t < T; ++t) {
+            h[k][t] = static_cast<Acc>(
+                __ldg(taps + static_cast<size_t>(t) * N + k * (N / R) + rank * RUN + j));
+            float2 x = make_float2(0.f, 0.f);
+            if (t >= 1 && rows > 0)
+                x = __ldg(gsrc + static_cast<long long>(t - 1) * N + k * (N / R) + j);
+            xw[k][t].x = static_cast<Acc>(x.x);
+            xw[k][t].y = static_cast<Acc>(x.y);
+        }
+    }
+    float4 twr[R > 1 ? R - 1 : 1];
+#pragma unroll
+    for (int i = 0; i + 1 < R; ++i)
+        twr[i] = __ldg(tw_g + i);
+
+    // tile slot offsets (float2 units) of this thread's channels
+    unsigned slot_of[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k)
+        slot_of[k] = sw(static_cast<unsigned>(k * (N / R) + rank * RUN + j));
+    const uint32_t tiles_u32 = smem_u32(tiles);
+    const uint32_t full_u32 = smem_u32(full);
+
+    for (long long b0 = 0; b0 < n_batches; b0 += BU) {
+#pragma unroll
+        for (int u = 0; u < BU; ++u) {
+            const long long b = b0 + u;
+            const long long f = b / Q;            // owner's fill index
+            const int d = static_cast<int>(b - f * Q); // owner CTA
+            const int t = static_cast<int>(f & 1);     // owner's tile
+            if (tid == 0) PPFG_TR(0, b, 0);
+            if (f >= 2)
+                mbar_wait(empty + d * 2 + t, static_cast<uint32_t>(((f >> 1) - 1) & 1));
+            if (tid == 0) PPFG_TR(0, b, 1);
+            const bool local = (static_cast<uint32_t>(d) == rank);
+            const uint32_t tile_u32 = tiles_u32 + static_cast<uint32_t>(t * Cfg::TILE_BYTES);
+            const uint32_t rtile = mapa(tile_u32, static_cast<uint32_t>(d));
+            const uint32_t rbar = mapa(full_u32 + t * 8u, static_cast<uint32_t>(d));
+            constexpr int CPB = B / Cfg::RB;       // chunks per batch
+            const long long c0 = b * CPB;         // this batch's chunks c0 .. c0+CPB-1
+            if (producer) {
+                // refill every slot released by the previous batches (all FIR
+                // warps are done with chunks < c0 once they have arrived).
+                // No proxy fence: the slot's last generic accesses are reads
+                // ordered by the empty mbarrier (as in CUTLASS's TMA
+                // pipelines), and a fence here would wait for this thread's
+                // outstanding DSMEM stores.
+#ifdef PPFG_TRACE
+                unsigned long long spins = 0, tq0 = gtimer();
+#endif
+                {
+                    int ws = rslot;
+                    uint32_t wp = rphase;
+                    for (long long q = rc; q < n_chunks && q < c0 + PC; ++q) {
+#ifdef PPFG_TRACE
+                        while (!mbar_test_wait(ring_empty + ws, wp))
+                            ++spins;
+#else
+                        mbar_wait(ring_empty + ws, wp);
+#endif
+                        if (++ws == PC) {
+                            ws = 0;
+                            wp ^= 1u;
+                        }
+                    }
+                }
+                PPFG_TR(0, b, 5);
+#ifdef PPFG_TRACE
+                if (blockIdx.x == 0 && b < 64) {
+                    g_trace[1][8][b] = spins + 1;
+                    g_trace[1][9][b] = rc;
+                    g_trace[1][10][b] = c0;
+                    g_trace[1][11][b] = tq0;
+                }
+#endif
+                while (rc < n_chunks && rc < c0 + PC) {
+                    issue(rc, rslot);
+                    ++rc;
+                    if (++rslot == PC) {
+                        rslot = 0;
+                        rphase ^= 1u;
+                    }
+                }
+            }
+            if (tid == 0) PPFG_TR(0, b, 4);
+            // wait for the batch's chunks up front, so the rows below form
+            // one straight-line block the scheduler can interleave
+            int slot[CPB];
+#pragma unroll
+            for (int i = 0; i < CPB; ++i) {
+                slot[i] = cslot;
+                if (c0 + i < n_chunks)
+                    mbar_wait(ring_full + cslot, cphase);
+                if (++cslot == PC) {
+                    cslot = 0;
+                    cphase ^= 1u;
+                }
+            }
+            const uint32_t ltile_u32 = tile_u32;
+            if (tid == 0) PPFG_TR(0, b, 2);
+            if (tid == 224) PPFG_TR(0, b, 6);
+#pragma unroll
+            for (int i = 0; i < B; ++i) {
+                const float2* chunk = ring + slot[i / Cfg::RB] * Cfg::CHUNK_FLOATS2 +
+                                      (i % Cfg::RB) * (R * RUN) + j;
+                float2 y[R];
+#pragma unroll
+                for (int k = 0; k < R; ++k) {
+                    const float2 x = chunk[k * RUN];
+#pragma unroll
+                    for (int tt = 0; tt + 1 < T; ++tt)
+                        xw[k][tt] = xw[k][tt + 1];
+                    xw[k][T - 1].x = static_cast<Acc>(x.x);
+                    xw[k][T - 1].y = static_cast<Acc>(x.y);
+                    if constexpr (Cfg::EXACT) {
+                        double ar = __dmul_rn(h[k][0], xw[k][0].x);
+                        double ai = __dmul_rn(h[k][0], xw[k][0].y);
+#pragma unroll
+                        for (int tt = 1; tt < T; ++tt) {
+                            ar = __fma_rn(h[k][tt], xw[k][tt].x, ar);
+                            ai = __fma_rn(h[k][tt], xw[k][tt].y, ai);
+                        }
+                        y[k] = make_float2(__double2float_rn(ar), __double2float_rn(ai));
+                    } else {
+                        float2 acc = mul2s(h[k][0], xw[k][0]);
+#pragma unroll
+                        for (int tt = 1; tt < T; ++tt)
+                            acc = fma2s(h[k][tt], xw[k][tt], acc);
+                        y[k] = acc;
+                    }
+                }
+                fft_prestages<Cfg::L, RLOG>(y, twr);
+#pragma unroll
+                for (int k = 0; k < R; ++k) {
+                    const uint32_t off = 8u * (i * Cfg::STRIDE + slot_of[k]);
+                    st_local_or_async_f2(local, ltile_u32 + off, rtile + off, y[k], rbar);
+                }
+            }
+            if (tid == 0) PPFG_TR(0, b, 3);
+            if (tid == 224) PPFG_TR(0, b, 7);
+            __syncwarp();
+            if (warp_leader) { // this warp is done with the batch's chunks
+#pragma unroll
+                for (int i = 0; i < CPB; ++i)
+                    if (c0 + i < n_chunks)
+                        mbar_arrive_relaxed(ring_empty + slot[i]);
+                PPFG_TR(0, b, 8 + tid / 32);
+            }
+            if (local)
+                named_arrive(1 + t, NFIR + NFFT); // own block of tile t written
+        }
+    }
+    cluster_sync_all();
+}
+
+} // namespace ppfg

@@ -2,7 +2,9 @@
 // device-resident streaming state, multi-GPU sharding and the C-ABI of
 // include/ppfg.h. Kernels live in fir.cuh (K1), fft.cuh (K2), fused.cuh (K3),
 // dft.cuh (K4 dft_naive, K5 synth).
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <atomic>
 #include <cmath>
@@ -21,6 +23,7 @@
 #include "fir.cuh"
 #include "fused.cuh"
 #include "fused_cluster.cuh"
+#include "fused_split.cuh"
 
 namespace {
 
@@ -95,6 +98,9 @@ struct FusedEntry {
     int rows_per_batch; // B * G
     int q;              // CTAs per cluster (1: single-SM kernel)
     bool preferred;     // cluster kernels: faster than FIR -> HBM -> FFT (measured)
+    int map_r = 0;      // > 0: the kernel reads its input through a 3-D TMA tensor
+    int map_rb = 0;     //      map with box {map_run, map_r, map_rb} (fused_split.cuh)
+    int map_run = 0;
 };
 
 template <class Cfg>
@@ -107,6 +113,13 @@ template <class Cfg>
 FusedEntry cluster_entry(bool preferred) {
     return {Cfg::L,    Cfg::T,  Cfg::EXACT, reinterpret_cast<KernelFn>(&fused_cluster_kernel<Cfg>),
             Cfg::SMEM, Cfg::NT, Cfg::B * Cfg::G, Cfg::Q, preferred};
+}
+
+template <class Cfg>
+FusedEntry split_entry(bool preferred) {
+    return {Cfg::L,    Cfg::T,  Cfg::EXACT, reinterpret_cast<KernelFn>(&fused_split_kernel<Cfg>),
+            Cfg::SMEM, Cfg::NT, Cfg::B,     Cfg::Q,
+            preferred, Cfg::R,  Cfg::RB,    Cfg::RUN};
 }
 
 // Which (C, T) get a fused kernel. Register budget per SM ~ C * (3T fp32 |
@@ -132,6 +145,15 @@ const std::vector<FusedEntry>& fused_table() {
         fused_entry<FusedCfg<9, 1, 1, false>>(),
         fused_entry<FusedCfg<10, 1, 2, false>>(),
         fused_entry<FusedCfg<11, 1, 3, false, 160, 96, 3>>(),
+        // clusters, FIR split by channel block and FFT by spectrum (fused_split.cuh)
+        split_entry<SplitCfg<10, 1, 16, false>>(false),
+        split_entry<SplitCfg<10, 2, 32, false>>(false),
+        split_entry<SplitCfg<10, 1, 8, true>>(false),
+        split_entry<SplitCfg<10, 2, 16, true>>(false),
+        split_entry<SplitCfg<11, 1, 8, false>>(false),
+        split_entry<SplitCfg<11, 2, 8, true>>(false),
+        split_entry<SplitCfg<12, 2, 8, false>>(false),
+        split_entry<SplitCfg<13, 3, 8, false>>(false),
         // clusters (fused_cluster.cuh): C/Q channels per SM, DSMEM for the last log2 Q stages
         // (preferred = default where round-1 measurements beat FIR -> HBM -> FFT)
         cluster_entry<ClusterCfg<11, 1, 8, 2, false>>(false),
@@ -348,6 +370,35 @@ __global__ void fft_stage_kernel(float2* data, const float4* __restrict__ tw, in
     r[base + j + half] = hi;
 }
 
+// Input view of the split kernel's TMA copies: 8-byte elements (c64 bytes,
+// moved untouched), dims {C/R channels, R runs, S_in spectra}; a box
+// {RUN, R, RB} at {rank*RUN, 0, row} is RB spectra x R runs of RUN channels.
+int encode_input_map(CUtensorMap* map, const float2* din, uint64_t C, uint64_t S_in, int r, int rb,
+                     int run) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    if (!encode)
+        return fail(PPFG_CUDA_ERROR, "cuTensorMapEncodeTiled is not available from the driver");
+    const cuuint64_t dims[3] = {C / r, static_cast<cuuint64_t>(r), S_in};
+    const cuuint64_t strides[2] = {C / r * sizeof(float2), C * sizeof(float2)};
+    const cuuint32_t box[3] = {static_cast<cuuint32_t>(run), static_cast<cuuint32_t>(r),
+                               static_cast<cuuint32_t>(rb)};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult res = encode(map, CU_TENSOR_MAP_DATA_TYPE_INT64, 3, const_cast<float2*>(din), dims,
+                                strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (res != CUDA_SUCCESS)
+        return fail(PPFG_CUDA_ERROR, "cuTensorMapEncodeTiled failed (" + std::to_string(res) + ")");
+    return PPFG_OK;
+}
+
 int launch_fused_entry(ppfg_plan p, const FusedEntry* e, const float* taps, uint64_t T,
                        const float2* din, uint64_t S_in, float2* dout, cudaStream_t st) {
     PPFG_TRY(ensure_smem_attr(e->fn, e->smem, p->device));
@@ -375,6 +426,13 @@ int launch_fused_entry(ppfg_plan p, const FusedEntry* e, const float* taps, uint
             1, std::min<uint64_t>(max_clusters, cdiv(S_out, e->rows_per_batch)));
         cfg.gridDim = dim3(static_cast<unsigned>(n_clusters * e->q));
         long long rows_per_cluster = static_cast<long long>(cdiv(S_out, n_clusters));
+        if (e->map_r > 0) {
+            CUtensorMap map;
+            PPFG_TRY(encode_input_map(&map, din, p->C, S_in, e->map_r, e->map_rb, e->map_run));
+            void* args[] = {&map, &din, &dout, &S_out_ll, &rows_per_cluster, &taps, &p->d_tw};
+            PPFG_CUDA(cudaLaunchKernelExC(&cfg, e->fn, args));
+            return check_launch("fused split fir+fft kernel");
+        }
         void* args[] = {&din, &dout, &S_out_ll, &rows_per_cluster, &taps, &p->d_tw};
         PPFG_CUDA(cudaLaunchKernelExC(&cfg, e->fn, args));
         return check_launch("fused cluster fir+fft kernel");
