@@ -58,9 +58,10 @@ typedef enum { PPFG_MEM_HOST = 0, PPFG_MEM_DEVICE = 1 } ppfg_mem;
  * fused FIR+FFT kernel accumulate the FIR in FP32 (max|err|/RMS well inside the
  * north-star 1e-5*log2(C) bound; FIR-only calls stay exact). PPFG_UNFUSED
  * forces FIR -> HBM -> FFT even where a fused kernel exists (for comparison).
- * PPFG_CLUSTER forces the thread-block-cluster fused kernels (C >= 2048,
- * T >= 16, FP64 at C = 1024); by default they are used only for the shapes
- * where they measured faster than the unfused path (T = 16, 32 at C = 1024). */
+ * PPFG_CLUSTER also admits the thread-block-cluster fused kernels that are
+ * not taken by default (C = 8192); the others (C = 2048, 4096; T = 16, 32 at
+ * C = 1024; FP64 at C = 1024, 2048) are used whenever they apply, since they
+ * measured faster than the unfused path. */
 enum {
     PPFG_EXACT = 0u,
     PPFG_FAST = 1u,

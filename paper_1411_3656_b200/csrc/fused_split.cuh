@@ -31,7 +31,7 @@
 
 #include <cuda.h>
 
-#include "fused_cluster.cuh"
+#include "cluster.cuh"
 
 namespace ppfg {
 
@@ -297,35 +297,8 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
                 // ordered by the empty mbarrier (as in CUTLASS's TMA
                 // pipelines), and a fence here would wait for this thread's
                 // outstanding DSMEM stores.
-#ifdef PPFG_TRACE
-                unsigned long long spins = 0, tq0 = gtimer();
-#endif
-                {
-                    int ws = rslot;
-                    uint32_t wp = rphase;
-                    for (long long q = rc; q < n_chunks && q < c0 + PC; ++q) {
-#ifdef PPFG_TRACE
-                        while (!mbar_test_wait(ring_empty + ws, wp))
-                            ++spins;
-#else
-                        mbar_wait(ring_empty + ws, wp);
-#endif
-                        if (++ws == PC) {
-                            ws = 0;
-                            wp ^= 1u;
-                        }
-                    }
-                }
-                PPFG_TR(0, b, 5);
-#ifdef PPFG_TRACE
-                if (blockIdx.x == 0 && b < 64) {
-                    g_trace[1][8][b] = spins + 1;
-                    g_trace[1][9][b] = rc;
-                    g_trace[1][10][b] = c0;
-                    g_trace[1][11][b] = tq0;
-                }
-#endif
                 while (rc < n_chunks && rc < c0 + PC) {
+                    mbar_wait(ring_empty + rslot, rphase);
                     issue(rc, rslot);
                     ++rc;
                     if (++rslot == PC) {
@@ -350,7 +323,6 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
             }
             const uint32_t ltile_u32 = tile_u32;
             if (tid == 0) PPFG_TR(0, b, 2);
-            if (tid == 224) PPFG_TR(0, b, 6);
 #pragma unroll
             for (int i = 0; i < B; ++i) {
                 const float2* chunk = ring + slot[i / Cfg::RB] * Cfg::CHUNK_FLOATS2 +
@@ -389,14 +361,12 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
                 }
             }
             if (tid == 0) PPFG_TR(0, b, 3);
-            if (tid == 224) PPFG_TR(0, b, 7);
             __syncwarp();
             if (warp_leader) { // this warp is done with the batch's chunks
 #pragma unroll
                 for (int i = 0; i < CPB; ++i)
                     if (c0 + i < n_chunks)
                         mbar_arrive_relaxed(ring_empty + slot[i]);
-                PPFG_TR(0, b, 8 + tid / 32);
             }
             if (local)
                 named_arrive(1 + t, NFIR + NFFT); // own block of tile t written

@@ -1,7 +1,8 @@
 // ppfg.cu — libppfg.so: plans, kernel dispatch, the host-streamed pipeline,
 // device-resident streaming state, multi-GPU sharding and the C-ABI of
 // include/ppfg.h. Kernels live in fir.cuh (K1), fft.cuh (K2), fused.cuh (K3),
-// dft.cuh (K4 dft_naive, K5 synth).
+// fused_split.cuh (K3s, thread-block clusters), dft.cuh (K4 dft_naive,
+// K5 synth).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -22,7 +23,6 @@
 #include "fft.cuh"
 #include "fir.cuh"
 #include "fused.cuh"
-#include "fused_cluster.cuh"
 #include "fused_split.cuh"
 
 namespace {
@@ -110,12 +110,6 @@ FusedEntry fused_entry() {
 }
 
 template <class Cfg>
-FusedEntry cluster_entry(bool preferred) {
-    return {Cfg::L,    Cfg::T,  Cfg::EXACT, reinterpret_cast<KernelFn>(&fused_cluster_kernel<Cfg>),
-            Cfg::SMEM, Cfg::NT, Cfg::B * Cfg::G, Cfg::Q, preferred};
-}
-
-template <class Cfg>
 FusedEntry split_entry(bool preferred) {
     return {Cfg::L,    Cfg::T,  Cfg::EXACT, reinterpret_cast<KernelFn>(&fused_split_kernel<Cfg>),
             Cfg::SMEM, Cfg::NT, Cfg::B,     Cfg::Q,
@@ -145,24 +139,21 @@ const std::vector<FusedEntry>& fused_table() {
         fused_entry<FusedCfg<9, 1, 1, false>>(),
         fused_entry<FusedCfg<10, 1, 2, false>>(),
         fused_entry<FusedCfg<11, 1, 3, false, 160, 96, 3>>(),
-        // clusters, FIR split by channel block and FFT by spectrum (fused_split.cuh)
-        split_entry<SplitCfg<10, 1, 16, false>>(false),
-        split_entry<SplitCfg<10, 2, 32, false>>(false),
-        split_entry<SplitCfg<10, 1, 8, true>>(false),
-        split_entry<SplitCfg<10, 2, 16, true>>(false),
-        split_entry<SplitCfg<11, 1, 8, false>>(false),
-        split_entry<SplitCfg<11, 2, 8, true>>(false),
-        split_entry<SplitCfg<12, 2, 8, false>>(false),
+        // thread-block clusters, FIR split by channel block and FFT by
+        // spectrum (fused_split.cuh) — for FIR state that does not fit one SM.
+        // preferred = taken by default: measured faster than FIR -> HBM -> FFT
+        // (round 1, 1 GiB inputs: C=1024 T=16 0.62 vs 0.32 of HBM roofline,
+        // T=32 0.41 vs 0.18, FP64 T=8 0.62 vs 0.42, FP64 T=16 0.40 vs 0.32,
+        // C=2048 0.51 vs 0.42, FP64 C=2048 0.47 vs 0.42, C=4096 0.43 vs 0.38;
+        // C=8192 0.29 vs 0.32 stays opt-in via PPFG_CLUSTER)
+        split_entry<SplitCfg<10, 1, 16, false>>(true),
+        split_entry<SplitCfg<10, 2, 32, false>>(true),
+        split_entry<SplitCfg<10, 1, 8, true>>(true),
+        split_entry<SplitCfg<10, 2, 16, true>>(true),
+        split_entry<SplitCfg<11, 1, 8, false>>(true),
+        split_entry<SplitCfg<11, 2, 8, true>>(true),
+        split_entry<SplitCfg<12, 2, 8, false>>(true),
         split_entry<SplitCfg<13, 3, 8, false>>(false),
-        // clusters (fused_cluster.cuh): C/Q channels per SM, DSMEM for the last log2 Q stages
-        // (preferred = default where round-1 measurements beat FIR -> HBM -> FFT)
-        cluster_entry<ClusterCfg<11, 1, 8, 2, false>>(false),
-        cluster_entry<ClusterCfg<12, 2, 8, 2, false>>(false),
-        cluster_entry<ClusterCfg<13, 3, 8, 2, false>>(false),
-        cluster_entry<ClusterCfg<10, 1, 16, 1, false>>(true),
-        cluster_entry<ClusterCfg<10, 2, 32, 0, false>>(true),
-        cluster_entry<ClusterCfg<10, 1, 8, 1, true>>(false),
-        cluster_entry<ClusterCfg<11, 2, 8, 1, true>>(false),
     };
     return t;
 }

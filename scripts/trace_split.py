@@ -18,17 +18,13 @@ buf = np.zeros(2 * 16 * 64, np.uint64)
 _lib.load().ppfg_debug_trace(C.c_void_p(buf.ctypes.data))
 buf = buf.reshape(2, 16, 64).astype(np.int64)
 t0 = buf[:, :8][buf[:, :8] > 0].min()
-names = {0: ["start", "empty_ok", "ring_ok", "stored", "issued", "waited", "w7_ring_ok", "w7_stored"] + [f"rel_w{w}" for w in range(8)], 1: ["start", "local_ok", "remote_ok", "done"]}
+names = {0: ["start", "empty_ok", "ring_ok", "stored", "issued"], 1: ["start", "local_ok", "remote_ok", "done"]}
 ev = []
 for role in (0, 1):
     for e, nm in enumerate(names[role]):
         for b in range(64):
             if buf[role, e, b] > 0:
                 ev.append((buf[role, e, b] - t0, ["fir", "fft"][role], b, nm))
-for b in range(12):
-    print("b", b, "spins", buf[1, 8, b] - 1, "rc", buf[1, 9, b], "c0", buf[1, 10, b], "tq0", (buf[1, 11, b] - t0) / 1000)
-buf[1, 8:12] = 0
-ev = [e for e in ev if not (e[1] == "fft" and e[3] not in names[1])]
 ev.sort()
 for t, r, b, nm in ev[:160]:
     print(f"{t/1000:9.3f} us {r} b={b:2d} {nm}")
