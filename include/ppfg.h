@@ -125,6 +125,23 @@ int ppfg_channelize(ppfg_plan plan, const void* in, uint64_t n_rows, void* out,
 int ppfg_fir_fft(ppfg_plan plan, const void* in, uint64_t n_spectra_in, void* out, int mem,
                  void* cuda_stream);
 
+/* Downstream detection, the step after channelization: per-channel mean power
+ * as `ppf inspect` computes it (cmd_inspect, cli.hpp:307-317):
+ *   mean_power[c] = sum_s ((double)re^2 + (double)im^2) / n_spectra
+ * over n_spectra rows of channelized bins (ppfg_mean_power) or over the
+ * n_spectra_in - T + 1 output spectra of ppfg_fir_fft (ppfg_fir_fft_mean_power;
+ * where a fused kernel exists the bins never reach memory, so the pass only
+ * reads its input). mean_power holds C doubles, in the same memory kind as
+ * the input. Each power term is exact as in the reference; the sum is taken
+ * per CTA in spectrum order and then over CTAs in a fixed order, so results
+ * are deterministic and differ from the reference's single running sum only
+ * by summation order (relative error ~1e-15). n_spectra == 0 gives zeros
+ * (the reference prints no mean then). */
+int ppfg_mean_power(ppfg_plan plan, const void* bins, uint64_t n_spectra, double* mean_power,
+                    int mem, void* cuda_stream);
+int ppfg_fir_fft_mean_power(ppfg_plan plan, const void* in, uint64_t n_spectra_in,
+                            double* mean_power, int mem, void* cuda_stream);
+
 /* Which kernel ppfg_fir_fft will run for this plan: 0 = unfused FIR+FFT,
  * 1 = fused FP32-FIR, 2 = fused FP64 (bit-exact) FIR, 3 / 4 = the cluster
  * versions of 1 / 2. */

@@ -71,6 +71,7 @@ class _Port:
         L.ppfo_fft.argtypes = [_f32p, _sz]
         L.ppfo_channelize.argtypes = [_f32p, _sz, _sz, C.c_int, _f32p]
         L.ppfo_fir_fft.argtypes = [_f32p, _sz, _sz, _sz, _f64p, C.c_int, _f32p]
+        L.ppfo_mean_power.argtypes = [_f32p, _sz, _sz, _f64p]
         L.ppfo_process_stream.argtypes = [_sz, _sz, _sz, C.c_int, C.c_int, C.c_void_p, _u8p, _sz,
                                           _u8p, C.POINTER(StreamState)]
         L.ppfo_bessel_i0.argtypes = [C.c_double, C.POINTER(C.c_int)]
@@ -121,6 +122,12 @@ class _Port:
         out = np.empty(max(s_in - T + 1, 0) * C_ * 2, np.float32)
         self._chk(self.lib.ppfo_fir_fft(x, s_in, C_, T, np.ascontiguousarray(coeffs, np.float64),
                                         int(fft_fallback), out))
+        return out
+
+    def mean_power(self, bins, C_):
+        bins = _cf(bins).reshape(-1)
+        out = np.empty(C_, np.float64)
+        self._chk(self.lib.ppfo_mean_power(bins, bins.size // (2 * C_), C_, out))
         return out
 
     def process_stream(self, src: bytes, C_, T, block_spectra, coeffs, fft_fallback=True,

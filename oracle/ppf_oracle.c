@@ -481,3 +481,23 @@ done:
     free(filt);
     return st;
 }
+
+/* cli.hpp:307-317. The product (double)re*re is exact (24-bit mantissas), so
+ * whether a compiler contracts re*re + im*im into an fma does not change p. */
+int ppfo_mean_power(const float* bins, size_t n_spectra, size_t n_channels, double* mean) {
+    if (n_channels == 0)
+        return PPFO_CONFIG_ERROR;
+    for (size_t c = 0; c < n_channels; ++c)
+        mean[c] = 0.0;
+    for (size_t s = 0; s < n_spectra; ++s) {
+        for (size_t c = 0; c < n_channels; ++c) {
+            const double re = (double)bins[2 * (s * n_channels + c)];
+            const double im = (double)bins[2 * (s * n_channels + c) + 1];
+            mean[c] += re * re + im * im;
+        }
+    }
+    if (n_spectra != 0)
+        for (size_t c = 0; c < n_channels; ++c)
+            mean[c] /= (double)n_spectra;
+    return PPFO_OK;
+}

@@ -11,7 +11,7 @@
  * Parity of this restatement is pinned (tests/test_oracle.py) against:
  *   - the reference itself compiled from its own headers (oracle/_ref, built
  *     by oracle/Makefile from /root/reference) — bit-for-bit;
- *   - golden vectors generated from that build (tests/golden/*.npz, script
+ *   - golden vectors generated from that build (tests/golden/reference_vectors.npz, script
  *     tests/golden/make_golden.py);
  *   - the known-answer values the reference tests hard-code.
  *
@@ -72,6 +72,12 @@ int ppfo_channelize(const float* filtered, size_t n_rows, size_t n_channels, int
 /* fir then channelize, as composed at pipeline.hpp:125-127 */
 int ppfo_fir_fft(const float* in, size_t n_spectra_in, size_t n_channels, size_t n_taps,
                  const double* coeff_values, int fft_fallback, float* out);
+
+/* cmd_inspect's mean power (cli.hpp:307-317): mean[c] = sum over spectra
+ * (in order, one running double sum per channel) of
+ * (double)re*re + (double)im*im, divided by n_spectra (left 0 when
+ * n_spectra == 0). */
+int ppfo_mean_power(const float* bins, size_t n_spectra, size_t n_channels, double* mean);
 
 /* pipeline.hpp:89-200 over an in-memory byte source. The source is read in
  * requests of block_spectra*C*8 bytes, each satisfied in full until EOF

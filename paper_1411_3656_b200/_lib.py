@@ -33,6 +33,8 @@ SIGNATURES = {
     "ppfg_fir_reference_order": (C.c_int, [vp, vp, u64, vp, C.c_int, vp]),
     "ppfg_channelize": (C.c_int, [vp, vp, u64, vp, C.c_int, C.c_int, vp]),
     "ppfg_fir_fft": (C.c_int, [vp, vp, u64, vp, C.c_int, vp]),
+    "ppfg_mean_power": (C.c_int, [vp, vp, u64, vp, C.c_int, vp]),
+    "ppfg_fir_fft_mean_power": (C.c_int, [vp, vp, u64, vp, C.c_int, vp]),
     "ppfg_fir_fft_kind": (C.c_int, [vp]),
     "ppfg_fft": (C.c_int, [vp, u64, vp]),
     "ppfg_dft_naive": (C.c_int, [vp, u64, vp]),

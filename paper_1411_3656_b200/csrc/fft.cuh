@@ -94,10 +94,16 @@ struct FftSchedule {
 // map(r) gives the global row of tile row r, or -1 for a padding row.
 // gin/gout may alias (in-place channelize): every row is fully read before it is
 // written, with a barrier in between for multi-pass transforms.
-template <int L, int LO, int W, bool FIRST_GLOBAL, bool FINAL, bool TW_SMEM, int NT, class RowMap>
+// POWER (with FINAL): instead of storing the bins, add each bin's power
+// p = (double)re*re + (double)im*im (cli.hpp:307-317) to the thread's
+// accumulators pacc[k] — the caller guarantees one unit per thread, so
+// pacc[k] always belongs to the same tile row and bin.
+template <int L, int LO, int W, bool FIRST_GLOBAL, bool FINAL, bool TW_SMEM, int NT, bool POWER = false,
+          class RowMap>
 PPFG_DEV void fft_tile_pass(const float2* gin, float2* gout,
                             float2* __restrict__ tile, unsigned row_stride, int rows,
-                            const RowMap& map, const float4* __restrict__ tw, int tid) {
+                            const RowMap& map, const float4* __restrict__ tw, int tid,
+                            double* pacc = nullptr) {
     constexpr int N = 1 << L;
     constexpr int E = 1 << W;
     constexpr int HI = LO + W - 1;
@@ -133,7 +139,14 @@ PPFG_DEV void fft_tile_pass(const float2* gin, float2* gout,
                 v[k] = src[sw(static_cast<unsigned>(k) << LO)];
         }
         fft_stages<L, LO, W, TW_SMEM>(v, fixed, tw);
-        if constexpr (FINAL) {
+        if constexpr (FINAL && POWER) {
+            if (map(r) >= 0) {
+#pragma unroll
+                for (int k = 0; k < E; ++k)
+                    pacc[k] += static_cast<double>(v[k].x) * v[k].x +
+                               static_cast<double>(v[k].y) * v[k].y;
+            }
+        } else if constexpr (FINAL) {
             const long long grow = map(r);
             if (grow >= 0) {
                 float2* dst = gout + grow * N + u;
@@ -158,23 +171,25 @@ PPFG_DEV void fft_tile_pass(const float2* gin, float2* gout,
 // STORE_LAST = false keeps the last pass's results in the tile (swizzled, by
 // label) instead of storing bins to global — used when more stages follow
 // (the cluster kernel's cross-CTA stages).
+// POWER: the last pass accumulates bin powers into pacc (see fft_tile_pass).
 template <int L, int LREM, int W, bool FIRST_GLOBAL, bool TW_SMEM, int NT, int I = 0,
-          bool STORE_LAST = true>
+          bool STORE_LAST = true, bool POWER = false>
 struct FftPasses {
     using S = FftSchedule<LREM, W>;
     static constexpr int WI = S::width(I);
     static constexpr int LO = S::lo(I);
     static constexpr bool LAST = (I == S::NP - 1);
+    static constexpr int E_LAST = 1 << S::width(S::NP - 1); // values per unit in the last pass
     template <class RowMap, class Sync>
     PPFG_DEV static void run(const float2* gin, float2* gout, float2* tile, unsigned row_stride,
                              int rows, const RowMap& map, const float4* tw, int tid,
-                             const Sync& sync) {
-        fft_tile_pass<L, LO, WI, FIRST_GLOBAL && I == 0, LAST && STORE_LAST, TW_SMEM, NT>(
-            gin, gout, tile, row_stride, rows, map, tw, tid);
+                             const Sync& sync, double* pacc = nullptr) {
+        fft_tile_pass<L, LO, WI, FIRST_GLOBAL && I == 0, LAST && STORE_LAST, TW_SMEM, NT,
+                      LAST && POWER>(gin, gout, tile, row_stride, rows, map, tw, tid, pacc);
         if constexpr (!LAST) {
             sync();
-            FftPasses<L, LREM, W, FIRST_GLOBAL, TW_SMEM, NT, I + 1, STORE_LAST>::run(
-                gin, gout, tile, row_stride, rows, map, tw, tid, sync);
+            FftPasses<L, LREM, W, FIRST_GLOBAL, TW_SMEM, NT, I + 1, STORE_LAST, POWER>::run(
+                gin, gout, tile, row_stride, rows, map, tw, tid, sync, pacc);
         }
     }
 };

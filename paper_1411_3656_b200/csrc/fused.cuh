@@ -120,7 +120,11 @@ PPFG_DEV void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-template <class Cfg>
+// POWER = true: the detection variant (cli.hpp:307-317 fused into the final
+// FFT pass): no bins are written; each FFT thread accumulates the powers of
+// the bins it owns over all of the CTA's spectra and `out` receives per-CTA
+// partial sums, double[gridDim.x][TILE_ROWS][N] (reduced by power_reduce_kernel).
+template <class Cfg, bool POWER = false>
 __global__ void __launch_bounds__(Cfg::NT, 1)
     fused_fir_fft_kernel(const float2* __restrict__ in, float2* __restrict__ out,
                          long long S_out, long long rows_per_cta, const float* __restrict__ taps,
@@ -158,14 +162,32 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
         // ================================ FFT role ================================
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(Cfg::FFT_REGS));
         const int ftid = tid - NFIR;
+        using Passes = FftPasses<L, L - RLOG, Cfg::W, false, true, NFFT, 0, true, POWER>;
+        constexpr int EL = Passes::E_LAST;
+        double pacc[POWER ? EL : 1];
+#pragma unroll
+        for (int k = 0; k < (POWER ? EL : 1); ++k)
+            pacc[k] = 0.0;
         for (long long b = 0; b < n_batches; ++b) {
             const int t = static_cast<int>(b & 1);
             named_sync(1 + t, NT);
-            FftPasses<L, L - RLOG, Cfg::W, false, true, NFFT>::run(
-                nullptr, out, tiles + t * Cfg::TILE_ROWS * Cfg::STRIDE, Cfg::STRIDE,
-                static_cast<int>(Cfg::TILE_ROWS), FusedRows{o0, o1, rpg, b * B, B}, tw, ftid,
-                SyncNamed{5, NFFT});
+            Passes::run(nullptr, out, tiles + t * Cfg::TILE_ROWS * Cfg::STRIDE, Cfg::STRIDE,
+                        static_cast<int>(Cfg::TILE_ROWS), FusedRows{o0, o1, rpg, b * B, B}, tw,
+                        ftid, SyncNamed{5, NFFT}, pacc);
             named_arrive(3 + t, NT);
+        }
+        if constexpr (POWER) {
+            // the last pass gives thread ftid exactly one unit: tile row r,
+            // bins u + rev_L(k)
+            constexpr int UL = N / EL;
+            static_assert(Cfg::TILE_ROWS * UL == NFFT, "one last-pass unit per FFT thread");
+            const int r = ftid / UL;
+            const unsigned u = static_cast<unsigned>(ftid % UL);
+            double* part = reinterpret_cast<double*>(out) +
+                           (static_cast<size_t>(blockIdx.x) * Cfg::TILE_ROWS + r) * N + u;
+#pragma unroll
+            for (int k = 0; k < EL; ++k)
+                part[crev(static_cast<unsigned>(k), L)] = pacc[k];
         }
         return;
     }
@@ -285,6 +307,49 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
                 mbar_arrive(empty_g + slot); // this warp is done with the chunk
             named_arrive(1 + t, NT);         // tile t is full
         }
+    }
+}
+
+// Per-channel mean power from per-CTA partials: mean[c] = (sum over parts,
+// in a fixed order) / n — deterministic for a given grid.
+__global__ void power_reduce_kernel(const double* __restrict__ part, int n_parts, int C,
+                                    double n, double* __restrict__ mean) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= C)
+        return;
+    double s = 0.0;
+    for (int i = 0; i < n_parts; ++i)
+        s += part[static_cast<size_t>(i) * C + c];
+    mean[c] = n > 0 ? s / n : 0.0;
+}
+
+// cmd_inspect on channelized bins (cli.hpp:307-317): CTA g sums the powers of
+// spectra [g*rows_per_cta, ...) per channel (thread = channel stripe), in
+// spectrum order, into part[g][c].
+__global__ void __launch_bounds__(256) power_partial_kernel(const float2* __restrict__ bins,
+                                                            long long n_spectra, int C,
+                                                            long long rows_per_cta,
+                                                            double* __restrict__ part) {
+    const long long s0 = static_cast<long long>(blockIdx.x) * rows_per_cta;
+    const long long s1 = min(s0 + rows_per_cta, n_spectra);
+    for (int c = threadIdx.x; c < C; c += blockDim.x) {
+        double acc = 0.0;
+        const float2* p = bins + s0 * C + c;
+        long long s = s0;
+        for (; s + 8 <= s1; s += 8, p += 8 * static_cast<long long>(C)) {
+            float2 a[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                a[i] = __ldcs(p + i * static_cast<long long>(C));
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                acc += static_cast<double>(a[i].x) * a[i].x + static_cast<double>(a[i].y) * a[i].y;
+        }
+        for (; s < s1; ++s, p += C) {
+            const float2 a = __ldcs(p);
+            acc += static_cast<double>(a.x) * a.x + static_cast<double>(a.y) * a.y;
+        }
+        part[static_cast<size_t>(blockIdx.x) * C + c] = acc;
     }
 }
 

@@ -101,12 +101,27 @@ struct FusedEntry {
     int map_r = 0;      // > 0: the kernel reads its input through a 3-D TMA tensor
     int map_rb = 0;     //      map with box {map_run, map_r, map_rb} (fused_split.cuh)
     int map_run = 0;
+    KernelFn power_fn = nullptr; // detection variant (POWER), single-SM entries
+    int power_rows = 0;          // its partials per CTA (tile rows)
 };
+
+// The detection variant exists where the last FFT pass gives every FFT thread
+// exactly one unit (its accumulators then always see the same bins).
+template <class Cfg>
+constexpr bool has_power() {
+    using P = FftPasses<Cfg::L, Cfg::L - Cfg::RLOG, Cfg::W, false, true, Cfg::NFFT, 0, true, true>;
+    return Cfg::T > 1 && Cfg::TILE_ROWS * (Cfg::N / P::E_LAST) == Cfg::NFFT;
+}
 
 template <class Cfg>
 FusedEntry fused_entry() {
-    return {Cfg::L,    Cfg::T,  Cfg::EXACT, reinterpret_cast<KernelFn>(&fused_fir_fft_kernel<Cfg>),
-            Cfg::SMEM, Cfg::NT, Cfg::B * Cfg::G, 1, true};
+    FusedEntry e{Cfg::L,    Cfg::T,  Cfg::EXACT, reinterpret_cast<KernelFn>(&fused_fir_fft_kernel<Cfg>),
+                 Cfg::SMEM, Cfg::NT, Cfg::B * Cfg::G, 1, true};
+    if constexpr (has_power<Cfg>()) {
+        e.power_fn = reinterpret_cast<KernelFn>(&fused_fir_fft_kernel<Cfg, true>);
+        e.power_rows = static_cast<int>(Cfg::TILE_ROWS);
+    }
+    return e;
 }
 
 template <class Cfg>
@@ -261,6 +276,11 @@ struct ppfg_plan_s {
     size_t h_in_bytes = 0, h_out_bytes = 0;
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
     cudaEvent_t ev_h2d[2] = {}, ev_comp[2] = {}, ev_d2h[2] = {};
+    // detection: per-CTA partial power sums (grow-only)
+    double* d_part = nullptr;
+    size_t part_bytes = 0;
+    void* d_bins = nullptr; // bins of the unfused detection path
+    size_t bins_bytes = 0;
 };
 
 namespace {
@@ -522,6 +542,115 @@ int launch_fir_fft(ppfg_plan p, const float2* din, uint64_t S_in, float2* dout, 
         return launch_fused(p, din, S_in, dout, st);
     PPFG_TRY(launch_fir(p, din, S_in, dout, st, false));
     return launch_channelize(p, dout, S_in - p->T + 1, dout, true, st);
+}
+
+// -------------------------------------------------------------- detection
+// Per-channel mean power of channelized spectra, cmd_inspect (cli.hpp:307-317):
+// mean[c] = sum_s ((double)re^2 + (double)im^2) / n. Partial sums per CTA in
+// spectrum order, then a fixed-order sum over CTAs: deterministic; it differs
+// from the reference's single running sum only by summation order (relative
+// ~1e-16 per term).
+int ensure_parts(ppfg_plan p, size_t bytes) {
+    if (p->part_bytes >= bytes)
+        return PPFG_OK;
+    cudaFree(p->d_part);
+    p->d_part = nullptr;
+    p->part_bytes = 0;
+    PPFG_CUDA(cudaMalloc(&p->d_part, bytes));
+    p->part_bytes = bytes;
+    return PPFG_OK;
+}
+
+int launch_power_reduce(ppfg_plan p, int n_parts, uint64_t n, double* dmean, cudaStream_t st) {
+    const int C = static_cast<int>(p->C);
+    power_reduce_kernel<<<static_cast<unsigned>(cdiv(p->C, 256)), 256, 0, st>>>(
+        p->d_part, n_parts, C, static_cast<double>(n), dmean);
+    return check_launch("power reduce kernel");
+}
+
+int launch_mean_power(ppfg_plan p, const float2* bins, uint64_t n, double* dmean, cudaStream_t st) {
+    const uint64_t grid = std::max<uint64_t>(
+        1, std::min<uint64_t>(static_cast<uint64_t>(p->num_sms) * 8, cdiv(n, 16)));
+    const long long rows = static_cast<long long>(cdiv(std::max<uint64_t>(n, 1), grid));
+    const int parts = static_cast<int>(cdiv(std::max<uint64_t>(n, 1), static_cast<uint64_t>(rows)));
+    PPFG_TRY(ensure_parts(p, static_cast<size_t>(parts) * p->C * sizeof(double)));
+    power_partial_kernel<<<static_cast<unsigned>(parts), 256, 0, st>>>(
+        bins, static_cast<long long>(n), static_cast<int>(p->C), rows, p->d_part);
+    PPFG_TRY(check_launch("power partial kernel"));
+    return launch_power_reduce(p, parts, n, dmean, st);
+}
+
+// FIR -> FFT -> mean power. With a detection variant of the fused kernel the
+// bins never reach HBM (the pass is read-only: 8*C*S_in bytes); otherwise the
+// bins go through a temporary buffer.
+int launch_fir_fft_mean_power(ppfg_plan p, const float2* din, uint64_t S_in, double* dmean,
+                              cudaStream_t st) {
+    const uint64_t S_out = S_in - p->T + 1;
+    const FusedEntry* e = p->fused;
+    if (e && e->power_fn && !(p->flags & PPFG_UNFUSED)) {
+        PPFG_TRY(ensure_smem_attr(e->power_fn, e->smem, p->device));
+        const uint64_t grid =
+            std::max<uint64_t>(1, std::min<uint64_t>(p->num_sms, cdiv(S_out, e->rows_per_batch)));
+        long long rows_per_cta = static_cast<long long>(cdiv(S_out, grid));
+        long long S_out_ll = static_cast<long long>(S_out);
+        const int parts = static_cast<int>(grid) * e->power_rows;
+        PPFG_TRY(ensure_parts(p, static_cast<size_t>(parts) * p->C * sizeof(double)));
+        float2* part = reinterpret_cast<float2*>(p->d_part);
+        void* args[] = {&din, &part, &S_out_ll, &rows_per_cta, &p->d_taps, &p->d_tw};
+        PPFG_CUDA(cudaLaunchKernel(e->power_fn, dim3(static_cast<unsigned>(grid)), dim3(e->nt), args,
+                                   e->smem, st));
+        PPFG_TRY(check_launch("fused fir+fft+power kernel"));
+        return launch_power_reduce(p, parts, S_out, dmean, st);
+    }
+    // bins through a plan-owned (grow-only) buffer; the stream orders reuse
+    const size_t bytes = S_out * p->C * sizeof(float2);
+    if (p->bins_bytes < bytes) {
+        cudaFree(p->d_bins);
+        p->d_bins = nullptr;
+        p->bins_bytes = 0;
+        PPFG_CUDA(cudaMalloc(&p->d_bins, bytes));
+        p->bins_bytes = bytes;
+    }
+    float2* bins = static_cast<float2*>(p->d_bins);
+    PPFG_TRY(launch_fir_fft(p, din, S_in, bins, st));
+    return launch_mean_power(p, bins, S_out, dmean, st);
+}
+
+// host buffers: stage the input in device memory, run, read the C means back
+int run_mean_power(ppfg_plan p, bool fused, const void* in, uint64_t n_rows, double* mean, int mem,
+                   void* s) {
+    DeviceGuard dg(p->device);
+    cudaStream_t st;
+    stream_of(p, s, &st);
+    if (mem == PPFG_MEM_DEVICE)
+        return fused ? launch_fir_fft_mean_power(p, static_cast<const float2*>(in), n_rows, mean, st)
+                     : launch_mean_power(p, static_cast<const float2*>(in), n_rows, mean, st);
+    if (mem != PPFG_MEM_HOST)
+        return fail(PPFG_CONFIG_ERROR, "ppfg: unknown memory kind");
+    const size_t in_bytes = n_rows * p->C * sizeof(float2);
+    void* din = nullptr;
+    double* dmean = nullptr;
+    PPFG_CUDA(cudaMallocAsync(&din, std::max<size_t>(in_bytes, 1), st));
+    int rc = cudaMallocAsync(reinterpret_cast<void**>(&dmean), p->C * sizeof(double), st) == cudaSuccess
+                 ? PPFG_OK
+                 : fail(PPFG_CUDA_ERROR, "mean power: allocation failed");
+    if (rc == PPFG_OK && in_bytes)
+        rc = cudaMemcpyAsync(din, in, in_bytes, cudaMemcpyHostToDevice, st) == cudaSuccess
+                 ? PPFG_OK
+                 : fail(PPFG_CUDA_ERROR, "mean power: H2D copy failed");
+    if (rc == PPFG_OK)
+        rc = fused ? launch_fir_fft_mean_power(p, static_cast<const float2*>(din), n_rows, dmean, st)
+                   : launch_mean_power(p, static_cast<const float2*>(din), n_rows, dmean, st);
+    if (rc == PPFG_OK)
+        rc = cudaMemcpyAsync(mean, dmean, p->C * sizeof(double), cudaMemcpyDeviceToHost, st) ==
+                     cudaSuccess
+                 ? PPFG_OK
+                 : fail(PPFG_CUDA_ERROR, "mean power: D2H copy failed");
+    cudaFreeAsync(din, st);
+    cudaFreeAsync(dmean, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess && rc == PPFG_OK)
+        rc = fail(PPFG_CUDA_ERROR, "mean power: stream error");
+    return rc;
 }
 
 // ------------------------------------------------------ host-mode pipeline
@@ -835,6 +964,8 @@ int ppfg_plan_destroy(ppfg_plan p) {
     cudaFree(p->d_tw);
     cudaFree(p->d_roots);
     cudaFree(p->d_ones);
+    cudaFree(p->d_part);
+    cudaFree(p->d_bins);
     for (int i = 0; i < 2; ++i) {
         cudaFree(p->d_in[i]);
         cudaFree(p->d_out[i]);
@@ -903,6 +1034,22 @@ int ppfg_fir_fft(ppfg_plan p, const void* in, uint64_t n_spectra_in, void* out, 
     if (in == out)
         return fail(PPFG_CONFIG_ERROR, "fir_fft: input and output must not alias");
     return run(p, Op::FirFft, in, n_spectra_in, out, mem, cuda_stream, p->T - 1);
+}
+
+int ppfg_mean_power(ppfg_plan p, const void* bins, uint64_t n_spectra, double* mean_power,
+                    int mem, void* cuda_stream) {
+    PPFG_TRY(check_plan(p));
+    if ((n_spectra && !bins) || !mean_power)
+        return fail(PPFG_CONFIG_ERROR, "mean_power: null buffer");
+    return run_mean_power(p, false, bins, n_spectra, mean_power, mem, cuda_stream);
+}
+
+int ppfg_fir_fft_mean_power(ppfg_plan p, const void* in, uint64_t n_spectra_in, double* mean_power,
+                            int mem, void* cuda_stream) {
+    if (!mean_power)
+        return fail(PPFG_CONFIG_ERROR, "fir_fft_mean_power: null output");
+    PPFG_TRY(check_fir_input(p, in, n_spectra_in, mean_power));
+    return run_mean_power(p, true, in, n_spectra_in, mean_power, mem, cuda_stream);
 }
 
 static int one_row(const void* in, uint64_t n, void* out, bool fallback, const char* who) {

@@ -281,6 +281,31 @@ class Plan:
         """channelize_block(ppf_fir_optimized(x)) — fused where available."""
         return self._call(self._lib.ppfg_fir_fft, x, out, lambda s: s - self.n_taps + 1)
 
+    def _power(self, fn, x, rows):
+        b = _Buf(x)
+        if _is_torch(x):
+            import torch
+            out = torch.empty(self.n_channels, dtype=torch.float64, device=x.device)
+            optr = out.data_ptr()
+        else:
+            out = np.empty(self.n_channels, np.float64)
+            optr = out.ctypes.data
+        _check(fn(self._h, b.ptr, rows(b), optr, b.mem, b.stream))
+        return out
+
+    def mean_power(self, bins):
+        """Per-channel mean power of channelized spectra, as `ppf inspect`
+        computes it (cmd_inspect, cli.hpp:307-317): float64[C]."""
+        def rows(b):
+            if b.n % self.n_channels:
+                raise config_error("inspect: malformed channelized block")
+            return b.n // self.n_channels
+        return self._power(self._lib.ppfg_mean_power, bins, rows)
+
+    def fir_fft_mean_power(self, x):
+        """mean_power(fir_fft(x)) without writing the bins (fused detection)."""
+        return self._power(self._lib.ppfg_fir_fft_mean_power, x, self._rows)
+
 
 # ---- one-shot reference-style API ---------------------------------------------------
 def _coeff_plan(coeffs: FilterCoefficients, flags=EXACT, device=0):

@@ -9,6 +9,8 @@ after 2 warm-ups:
   fir         ppfg_fir (K1, bit-exact FP64 accumulation) alone
   fft         ppfg_channelize (K2, bit-exact radix-2) alone, in place
   cufft       torch.fft.fft over the same rows (cuFFT; comparison point only)
+  detect      ppfg_fir_fft_mean_power, PPFG_FAST (per-channel mean power; frac =
+              input bytes / time / peak, the pass being read-only when fused)
 GB/s = input bytes / time; roofline frac = (in + out bytes) / time / peak.
 Writes JSON lines to stdout and a markdown table to --md.
 """
@@ -59,6 +61,11 @@ def point(C, T, gib, peak):
             res[mode] = {"ms": t * 1e3, "gbs_in": bin_ / t / 1e9,
                          "frac": (bin_ + bout) / t / 1e9 / peak,
                          "kernel": ["unfused", "fused-fp32", "fused-fp64", "cluster-fp32", "cluster-fp64"][p.kind]}
+    with ppf.Plan(C, T, coeffs, flags=ppf.FAST) as p:
+        # detection (mean power per channel): only the input is HBM traffic
+        # when a fused detection kernel exists
+        t = timeit(lambda: p.fir_fft_mean_power(x))
+        res["detect"] = {"ms": t * 1e3, "gbs_in": bin_ / t / 1e9, "frac": bin_ / t / 1e9 / peak}
     with ppf.Plan(C, T, coeffs) as p:
         t = timeit(lambda: p.fir(x, out=y))
         res["fir"] = {"ms": t * 1e3, "gbs_in": bin_ / t / 1e9,
@@ -93,15 +100,17 @@ def main():
         with open(args.md, "w") as f:
             f.write(f"# Sweep ({args.gib} GiB input per point, HBM peak {peak} GB/s {src})\n\n")
             f.write("| C | T | fused FAST GB/s in (frac, kernel) | EXACT GB/s in (frac, kernel) | "
-                    "FIR-only GB/s in (frac) | FFT-only ms (frac) | cuFFT ms (frac) |\n")
-            f.write("|---|---|---|---|---|---|---|\n")
+                    "FIR-only GB/s in (frac) | FFT-only ms (frac) | cuFFT ms (frac) | "
+                    "detect FAST GB/s in (frac of read-only) |\n")
+            f.write("|---|---|---|---|---|---|---|---|\n")
             for r in rows:
                 f.write(f"| {r['C']} | {r['T']} | {r['fused_fast']['gbs_in']:.0f} "
                         f"({r['fused_fast']['frac']:.2f}, {r['fused_fast']['kernel']}) | "
                         f"{r['exact']['gbs_in']:.0f} ({r['exact']['frac']:.2f}, "
                         f"{r['exact']['kernel']}) | {r['fir']['gbs_in']:.0f} ({r['fir']['frac']:.2f})"
                         f" | {r['fft']['ms']:.3f} ({r['fft']['frac']:.2f}) | "
-                        f"{r['cufft']['ms']:.3f} ({r['cufft']['frac']:.2f}) |\n")
+                        f"{r['cufft']['ms']:.3f} ({r['cufft']['frac']:.2f}) | "
+                        f"{r['detect']['gbs_in']:.0f} ({r['detect']['frac']:.2f}) |\n")
 
 
 if __name__ == "__main__":

@@ -323,3 +323,55 @@ def test_host_pipeline_pinned_and_pageable(cuda, port):
     assert np.array_equal(bits(a[:3000 - T + 1]), bits(head))
     tail = port.fir_fft(x[-3000:], C, T, c.values)
     assert np.array_equal(bits(a[-(3000 - T + 1):]), bits(tail))
+
+
+# ------------------------------------------------- detection
+def _rel(got, want):
+    got, want = np.asarray(got, np.float64), np.asarray(want, np.float64)
+    return float(np.max(np.abs(got - want) / np.maximum(np.abs(want), 1e-300)))
+
+
+@pytest.mark.parametrize("C,S", [(1024, 5000), (64, 3), (12, 700), (1, 10), (4096, 300)])
+def test_mean_power_vs_oracle(cuda, port, C, S):
+    """ppfg_mean_power == cmd_inspect's running sum up to summation order."""
+    import torch
+    ppf = ppf_mod()
+    bins = uniform(np.random.default_rng(C + S), S * C).reshape(S, C)
+    want = port.mean_power(bins, C)
+    with ppf.Plan(C) as p:
+        got = p.mean_power(bins)
+        again = p.mean_power(bins)
+        dev = p.mean_power(torch.from_numpy(bins).cuda())
+        torch.cuda.synchronize()
+    assert _rel(got, want) <= 1e-13
+    assert np.array_equal(got, again)                 # deterministic
+    assert np.array_equal(dev.cpu().numpy(), got)     # host and device paths agree
+
+
+def test_mean_power_empty(cuda):
+    ppf = ppf_mod()
+    with ppf.Plan(16) as p:
+        assert np.array_equal(p.mean_power(np.zeros(0, np.complex64)), np.zeros(16))
+
+
+@pytest.mark.parametrize("C,T,flags", [(1024, 8, "fast"), (512, 8, "exact"), (1024, 4, "fast"),
+                                       (512, 16, "fast"), (1024, 16, "fast"), (100, 4, "exact"),
+                                       (2048, 8, "exact")])
+def test_fir_fft_mean_power(cuda, port, C, T, flags):
+    """Fused detection (bins never written where a detection kernel exists)
+    == mean_power(fir_fft(x)) == the oracle's inspect of the oracle's bins."""
+    ppf = ppf_mod()
+    S = T - 1 + 148 * 8 * 2 + 37
+    x = ppf.synth(C, S * C, seed=C + T)
+    coeffs = port.generate_prototype(C, T, 9.0)
+    f = ppf.FAST if flags == "fast" else ppf.EXACT
+    with ppf.Plan(C, T, coeffs, flags=f) as p:
+        fused = p.fir_fft_mean_power(x)
+        bins = p.fir_fft(x)
+        via_bins = p.mean_power(bins)
+    want = port.mean_power(port.fir_fft(x, C, T, coeffs), C)
+    assert _rel(fused, via_bins) <= 1e-13
+    if flags == "exact":
+        assert _rel(fused, want) <= 1e-13              # bins bit-exact: only the sum order differs
+    else:
+        assert _rel(fused, want) <= 2e-5 * np.log2(C)  # FP32 FIR: |X|^2 inherits 2x its error

@@ -115,3 +115,20 @@ def test_port_impulse_orientation(port):
                 assert y[s, cc] == np.float32(c[(pos - s) * C + cc])
             else:
                 assert y[s, cc] == 0
+
+
+def test_port_mean_power_is_the_inspect_running_sum(port):
+    """cmd_inspect (cli.hpp:307-317): one running double sum per channel, in
+    spectrum order, of (double)re^2 + (double)im^2, then / n."""
+    rng = np.random.default_rng(5)
+    C, S = 6, 37
+    x = uniform(rng, S * C).reshape(S, C)
+    want = np.zeros(C)
+    for s in range(S):
+        for c in range(C):
+            re, im = float(x[s, c].real), float(x[s, c].imag)
+            want[c] += re * re + im * im
+    want /= S
+    got = port.mean_power(x, C)
+    assert np.array_equal(got, want)
+    assert np.array_equal(port.mean_power(np.zeros(0, np.complex64), C), np.zeros(C))
