@@ -146,8 +146,14 @@ const std::vector<FusedEntry>& fused_table() {
         fused_entry<FusedCfg<10, 4, 2, false>>(),
         fused_entry<FusedCfg<9, 16, 1, false>>(),
         fused_entry<FusedCfg<9, 8, 1, true>>(),
+        fused_entry<FusedCfg<8, 8, 1, true>>(),
+        fused_entry<FusedCfg<7, 8, 1, true>>(),
+        fused_entry<FusedCfg<6, 8, 1, true>>(),
+        fused_entry<FusedCfg<10, 4, 2, true>>(),
         // T = 1 with unit taps: x*1 == x exactly, so these are bit-exact,
         // TMA-fed, warp-specialised FFTs — channelize_block for 64 <= C <= 2048
+        // (split-kernel T = 1 entries for C = 4096, 8192 and FP64 C = 4096 on
+        // 8-CTA clusters measured slower than K2 / the unfused path)
         fused_entry<FusedCfg<6, 1, 0, false, 120, 80, 2, 3>>(),
         fused_entry<FusedCfg<7, 1, 0, false, 120, 80, 2, 3>>(),
         fused_entry<FusedCfg<8, 1, 0, false>>(),
@@ -169,6 +175,7 @@ const std::vector<FusedEntry>& fused_table() {
         split_entry<SplitCfg<11, 2, 8, true>>(true),
         split_entry<SplitCfg<12, 2, 8, false>>(true),
         split_entry<SplitCfg<13, 3, 8, false>>(false),
+
     };
     return t;
 }

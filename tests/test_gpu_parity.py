@@ -131,9 +131,10 @@ def test_fft_api_semantics(cuda, port):
 def test_channelize_in_place_device(cuda, port):
     import torch
     ppf = ppf_mod()
-    for n in (6, 64, 1024, 32768):
-        rng = np.random.default_rng(n)
-        x = uniform(rng, 17 * n)
+    for n, rows in ((6, 17), (64, 17), (1024, 17), (2048, 301), (4096, 17), (4096, 733),
+                    (8192, 611), (32768, 17)):
+        rng = np.random.default_rng(n + rows)
+        x = uniform(rng, rows * n)
         t = torch.from_numpy(x.copy()).to(cuda)
         with ppf.Plan(n) as p:
             p.channelize(t, out=t)
