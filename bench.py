@@ -202,6 +202,22 @@ def run_reference_arm(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def ncu_traffic(C, T, mode, n_spectra_in):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
+    kernel, from the committed `ncu --set full` capture of this same
+    configuration (profiles/round1/traffic_*.json); None if there is none."""
+    import glob
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "traffic_*.json"))):
+        try:
+            t = json.load(open(f))
+        except (OSError, ValueError):
+            continue
+        if (t.get("n_channels"), t.get("n_taps"), t.get("mode"), t.get("n_spectra_in")) == \
+                (C, T, mode, n_spectra_in):
+            return t["traffic_per_launch"]
+    return None
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -357,6 +373,7 @@ def main():
 
     if rank == 0:
         kind = plan.kind
+        traffic = ncu_traffic(C, T, args.mode, ic)
         line = {
             "metric": METRIC,
             "value": value,
@@ -377,7 +394,7 @@ def main():
                        "mode": args.mode, "kernel": ["unfused", "fused-fp32", "fused-fp64", "cluster-fp32", "cluster-fp64"][kind],
                        "l2": "inputs >> 126 MB L2 (no flush needed)", "parallelism": f"shard{world}"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "bytes_per_launch": alg_bytes,
                          "launch_ms": t_launch * 1e3},
             "cpu_baseline": cpu,
