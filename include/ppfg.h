@@ -66,7 +66,9 @@ enum {
     PPFG_EXACT = 0u,
     PPFG_FAST = 1u,
     PPFG_UNFUSED = 2u,
-    PPFG_CLUSTER = 4u
+    PPFG_CLUSTER = 4u,
+    PPFG_K1_PREFETCH = 8u /* comparison only: FIR-only kernel with register prefetch
+                             instead of TMA-staged input (same results) */
 };
 
 typedef struct ppfg_plan_s* ppfg_plan;

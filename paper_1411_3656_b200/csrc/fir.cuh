@@ -19,6 +19,8 @@
 // unrolled by TC so the window is a circular register file (no moves).
 #pragma once
 
+#include <cuda.h>
+
 #include "common.cuh"
 
 namespace ppfg {
@@ -111,6 +113,145 @@ __global__ void __launch_bounds__(256) fir_chain_kernel(const float2* __restrict
             carry[u % LAG] = acc;
             const long long s = s0 + tau - static_cast<long long>(LAG) * qq;
             if (live && qq == K - 1 && q < K && tau < steps && s >= s0 && s < s1)
+                __stcs(out + s * C + c, make_float2(__double2float_rn(acc.x),
+                                                    __double2float_rn(acc.y)));
+        }
+    }
+}
+
+// K1t — the same warp tasks and op sequence as fir_chain_kernel, with the
+// input staged by TMA instead of register prefetch: each warp owns a private
+// ring of NS chunks (RB spectra x CPW channels, one 2-D tensor copy each,
+// SASS UTMALDG) in shared memory, refilled by its lane 0 as soon as the
+// warp's lane-0 tap chunk has read a chunk's last spectrum — no cross-warp
+// coupling. Freeing the prefetch registers lets two 8-warp blocks share an
+// SM (the register-prefetch kernel needs ~218 registers at TC = 16, one
+// block), and the ring keeps >= 2 chunks of lookahead in flight.
+template <int TC, int K, int LAG, int RB>
+struct FirTma {
+    static constexpr int CPW = 32 / K;
+    // rows a warp needs at once: the newest row of every tap chunk plus the
+    // window prefill, rounded to chunks, plus two chunks of lookahead
+    static constexpr int SPAN = TC - 1 + (K - 1) * (TC - LAG);
+    static constexpr int NS = (SPAN + TC) / RB + 3;
+    static constexpr size_t RING_FLOATS2 = size_t(NS) * RB * CPW;
+    static constexpr int WARPS = 8;
+    static constexpr size_t BAR_OFF = sizeof(float2) * RING_FLOATS2 * WARPS;
+    static constexpr size_t SMEM = BAR_OFF + sizeof(uint64_t) * NS * WARPS;
+};
+
+template <int TC, int K, int LAG, int RB, int MINB>
+__global__ void __launch_bounds__(256, MINB) fir_tma_kernel(const __grid_constant__ CUtensorMap map,
+                                                         float2* __restrict__ out, unsigned C,
+                                                         long long S_out,
+                                                         const float* __restrict__ taps, int seg,
+                                                         long long n_tasks, double init) {
+    using F = FirTma<TC, K, LAG, RB>;
+    constexpr int CPW = F::CPW, NS = F::NS;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    float2* ring = reinterpret_cast<float2*>(smem_raw) + warp * F::RING_FLOATS2;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + F::BAR_OFF) + warp * NS;
+    const long long task = static_cast<long long>(blockIdx.x) * F::WARPS + warp;
+    if (task >= n_tasks)
+        return; // warps are independent: no block-wide barrier below
+    const int q = lane / CPW;
+    const int cl = lane - q * CPW;
+    const long long n_cb = (C + CPW - 1) / CPW;
+    const long long sg = task / n_cb;
+    const unsigned c0 = static_cast<unsigned>((task - sg * n_cb) * CPW);
+    const unsigned c_raw = c0 + cl;
+    const bool live = q < K && c_raw < C;
+    const unsigned c = live ? c_raw : 0u;
+    const int qq = q < K ? q : K - 1;
+    const long long s0 = sg * seg;
+    const long long s1 = min(s0 + seg, S_out);
+    const int steps = static_cast<int>(s1 - s0) + LAG * (K - 1);
+    // relative rows rr = 0 .. n_rows-1 (absolute s0 + rr; TMA zero-fills past the input)
+    const int n_rows = steps + TC - 1 + (K - 1) * (TC - LAG);
+    const int n_chunks = (n_rows + RB - 1) / RB;
+
+    if (lane == 0) {
+        for (int i = 0; i < NS; ++i)
+            mbar_init(full + i, 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    auto issue = [&](int k) { // lane 0 only
+        const int slot = k % NS;
+        mbar_arrive_expect_tx(full + slot, static_cast<uint32_t>(sizeof(float2) * RB * CPW));
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(ring + slot * RB * CPW)),
+            "l"(reinterpret_cast<uint64_t>(&map)), "r"(static_cast<int>(c0)),
+            "r"(static_cast<int>(s0 + static_cast<long long>(k) * RB)), "r"(smem_u32(full + slot))
+            : "memory");
+    };
+    if (lane == 0)
+        for (int k = 0; k < NS && k < n_chunks; ++k)
+            issue(k);
+    int waited = 0;   // chunks [0, waited) have landed
+    int released = 0; // chunks [0, released) are consumed; issued = released + NS
+    auto wait_upto = [&](int rr) {
+        const int k1 = min(rr / RB, n_chunks - 1);
+        for (; waited <= k1; ++waited)
+            mbar_wait(full + waited % NS, static_cast<uint32_t>((waited / NS) & 1));
+    };
+    auto row = [&](int rr) { // this lane's channel of relative row rr
+        return ring[((rr / RB) % NS) * RB * CPW + (rr % RB) * CPW + cl];
+    };
+
+    double h[TC];
+#pragma unroll
+    for (int t = 0; t < TC; ++t)
+        h[t] = static_cast<double>(__ldg(taps + static_cast<size_t>(qq * TC + t) * C + c));
+
+    const int base = qq * (TC - LAG); // lane q's rows: base + tau + [0, TC)
+    wait_upto(base + TC - 2 + (K - 1 - qq) * (TC - LAG));
+    double2 w[TC];
+#pragma unroll
+    for (int t = 0; t + 1 < TC; ++t) {
+        const float2 x = row(base + t);
+        w[t] = make_double2(x.x, x.y);
+    }
+    const unsigned src_lane_off = CPW;
+    double2 carry[LAG];
+#pragma unroll
+    for (int i = 0; i < LAG; ++i)
+        carry[i] = make_double2(0.0, 0.0);
+    for (int tau0 = 0; tau0 < steps; tau0 += TC) {
+        // chunks wholly below lane 0's first read of this block were read
+        // (and converted) in earlier blocks: refill their slots
+        const int done = (tau0 + TC - 1) / RB;
+        __syncwarp();
+        for (; released < done; ++released)
+            if (lane == 0 && released + NS < n_chunks)
+                issue(released + NS);
+        wait_upto(tau0 + 2 * TC - 2 + (K - 1) * (TC - LAG));
+#pragma unroll
+        for (int u = 0; u < TC; ++u) {
+            const int tau = tau0 + u;
+            const float2 xn = row(base + tau + TC - 1);
+            w[(u + TC - 1) % TC] = make_double2(xn.x, xn.y);
+            double2 acc = make_double2(init, init);
+            if constexpr (K > 1) {
+                acc.x = __shfl_up_sync(0xffffffffu, carry[u % LAG].x, src_lane_off);
+                acc.y = __shfl_up_sync(0xffffffffu, carry[u % LAG].y, src_lane_off);
+                if (qq == 0) {
+                    acc.x = init;
+                    acc.y = init;
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < TC; ++t) {
+                const double2 v = w[(u + t) % TC];
+                acc.x = __fma_rn(h[t], v.x, acc.x);
+                acc.y = __fma_rn(h[t], v.y, acc.y);
+            }
+            carry[u % LAG] = acc;
+            const long long s = s0 + tau - static_cast<long long>(LAG) * qq;
+            if (live && qq == K - 1 && tau < steps && s >= s0 && s < s1)
                 __stcs(out + s * C + c, make_float2(__double2float_rn(acc.x),
                                                     __double2float_rn(acc.y)));
         }

@@ -223,6 +223,32 @@ FirEntry fir_entry() {
 
 // K1 variants: one lane per channel up to T = 16; larger T split over K
 // lanes of up to 16 taps (T = TC * K), chained with a lag (fir.cuh).
+struct FirTmaEntry {
+    KernelFn fn = nullptr;
+    int k = 0, rb = 0;
+    size_t smem = 0;
+};
+
+template <int TC, int K, int RB, int MINB = 2>
+FirTmaEntry fir_tma_entry() {
+    constexpr int LAG = K == 1 ? 1 : (TC % 4 == 0 ? 4 : (TC % 2 == 0 ? 2 : 1));
+    using F = FirTma<TC, K, LAG, RB>;
+    return {reinterpret_cast<KernelFn>(&fir_tma_kernel<TC, K, LAG, RB, MINB>), K, RB, F::SMEM};
+}
+
+// K1t shapes (TMA-staged input; measured FIR-only at C = 1024: T = 8 0.87 vs
+// 0.79, T = 16 0.66 vs 0.50 of the HBM roofline). The lane-chained shapes
+// (T > 16) stay on the register-prefetch K1, which measured faster there.
+FirTmaEntry fir_tma_table(int T) {
+    switch (T) {
+    case 4: return fir_tma_entry<4, 1, 8>();
+    case 8: return fir_tma_entry<8, 1, 8>();
+    case 12: return fir_tma_entry<12, 1, 8>();
+    case 16: return fir_tma_entry<16, 1, 8>();
+    default: return {};
+    }
+}
+
 FirEntry fir_table(int T) {
     switch (T) {
 #define PPFG_FIR(t, tc, k)                                                                        \
@@ -324,6 +350,8 @@ int stream_of(ppfg_plan p, void* s, cudaStream_t* out) {
 }
 
 // ---------------------------------------------------------- launchers (device)
+int encode_rows_map(CUtensorMap* map, const float2* din, uint64_t C, uint64_t S_in, int cpw, int rb);
+
 int launch_fir(ppfg_plan p, const float2* din, uint64_t S_in, float2* dout, cudaStream_t st,
                bool reference_order) {
     const uint64_t T = p->T, C = p->C;
@@ -331,6 +359,28 @@ int launch_fir(ppfg_plan p, const float2* din, uint64_t S_in, float2* dout, cuda
     const double init = reference_order ? 0.0 : -0.0;
     long long S_in_ll = static_cast<long long>(S_in), S_out_ll = static_cast<long long>(S_out);
     unsigned Cu = static_cast<unsigned>(C);
+    // TMA needs 16-byte-aligned rows (even C) and base address
+    const bool tma_ok = !(p->flags & PPFG_K1_PREFETCH) && (C % 2 == 0) &&
+                        (reinterpret_cast<uintptr_t>(din) % 16 == 0);
+    const FirTmaEntry et = tma_ok ? fir_tma_table(static_cast<int>(T)) : FirTmaEntry{};
+    if (et.fn) {
+        const uint64_t cpw = 32 / et.k;
+        const uint64_t n_cb = cdiv(C, cpw);
+        const uint64_t target_tasks = static_cast<uint64_t>(p->num_sms) * 16 * 4;
+        uint64_t seg = cdiv(S_out * n_cb, target_tasks);
+        seg = std::max<uint64_t>(seg, std::min<uint64_t>(std::max<uint64_t>(64, 4 * T), S_out));
+        const uint64_t n_seg = cdiv(S_out, seg);
+        long long n_tasks = static_cast<long long>(n_seg * n_cb);
+        int seg_i = static_cast<int>(seg);
+        const unsigned blocks = static_cast<unsigned>(cdiv(static_cast<uint64_t>(n_tasks), 8));
+        CUtensorMap map;
+        PPFG_TRY(encode_rows_map(&map, din, C, S_in, static_cast<int>(cpw), et.rb));
+        PPFG_TRY(ensure_smem_attr(et.fn, et.smem, p->device));
+        void* args[] = {&map, &dout, &Cu, &S_out_ll, &p->d_taps, &seg_i, &n_tasks,
+                        const_cast<double*>(&init)};
+        PPFG_CUDA(cudaLaunchKernel(et.fn, dim3(blocks), dim3(256), args, et.smem, st));
+        return check_launch("fir kernel (TMA)");
+    }
     const FirEntry e = fir_table(static_cast<int>(T));
     if (e.fn) {
         // warp tasks = (channel block of 32/K channels) x (time segment); segments
@@ -388,11 +438,7 @@ __global__ void fft_stage_kernel(float2* data, const float4* __restrict__ tw, in
     r[base + j + half] = hi;
 }
 
-// Input view of the split kernel's TMA copies: 8-byte elements (c64 bytes,
-// moved untouched), dims {C/R channels, R runs, S_in spectra}; a box
-// {RUN, R, RB} at {rank*RUN, 0, row} is RB spectra x R runs of RUN channels.
-int encode_input_map(CUtensorMap* map, const float2* din, uint64_t C, uint64_t S_in, int r, int rb,
-                     int run) {
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
         void* fn = nullptr;
         cudaDriverEntryPointQueryResult q;
@@ -401,6 +447,15 @@ int encode_input_map(CUtensorMap* map, const float2* din, uint64_t C, uint64_t S
             fn = nullptr;
         return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
     }();
+    return encode;
+}
+
+// Input view of the split kernel's TMA copies: 8-byte elements (c64 bytes,
+// moved untouched), dims {C/R channels, R runs, S_in spectra}; a box
+// {RUN, R, RB} at {rank*RUN, 0, row} is RB spectra x R runs of RUN channels.
+int encode_input_map(CUtensorMap* map, const float2* din, uint64_t C, uint64_t S_in, int r, int rb,
+                     int run) {
+    PFN_cuTensorMapEncodeTiled_v12000 encode = tensor_map_encoder();
     if (!encode)
         return fail(PPFG_CUDA_ERROR, "cuTensorMapEncodeTiled is not available from the driver");
     const cuuint64_t dims[3] = {C / r, static_cast<cuuint64_t>(r), S_in};
@@ -409,6 +464,25 @@ int encode_input_map(CUtensorMap* map, const float2* din, uint64_t C, uint64_t S
                                static_cast<cuuint32_t>(rb)};
     const cuuint32_t estr[3] = {1, 1, 1};
     const CUresult res = encode(map, CU_TENSOR_MAP_DATA_TYPE_INT64, 3, const_cast<float2*>(din), dims,
+                                strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (res != CUDA_SUCCESS)
+        return fail(PPFG_CUDA_ERROR, "cuTensorMapEncodeTiled failed (" + std::to_string(res) + ")");
+    return PPFG_OK;
+}
+
+// K1t input view: 8-byte elements, dims {C channels, S_in spectra}; a box
+// {cpw, rb} at {c0, row} is rb spectra of cpw consecutive channels.
+int encode_rows_map(CUtensorMap* map, const float2* din, uint64_t C, uint64_t S_in, int cpw, int rb) {
+    PFN_cuTensorMapEncodeTiled_v12000 encode = tensor_map_encoder();
+    if (!encode)
+        return fail(PPFG_CUDA_ERROR, "cuTensorMapEncodeTiled is not available from the driver");
+    const cuuint64_t dims[2] = {C, S_in};
+    const cuuint64_t strides[1] = {C * sizeof(float2)};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(cpw), static_cast<cuuint32_t>(rb)};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult res = encode(map, CU_TENSOR_MAP_DATA_TYPE_INT64, 2, const_cast<float2*>(din), dims,
                                 strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                 CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);

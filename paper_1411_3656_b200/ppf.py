@@ -20,6 +20,7 @@ EXACT = 0
 FAST = 1
 UNFUSED = 2
 CLUSTER = 4
+K1_PREFETCH = 8  # comparison only: register-prefetch FIR kernel
 MEM_HOST = 0
 MEM_DEVICE = 1
 

@@ -1,0 +1,18 @@
+"""Time K1 (FIR only, bit-exact) at C=1024 for a list of T on 1 GiB input."""
+import os, sys, json
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_1411_3656_b200 import ppf
+from scripts.sweep import timeit
+import bench
+peak, _ = bench.measured_peak()
+C = 1024
+for T in [int(t) for t in sys.argv[1].split(",")]:
+    S = (1 << 30) // (C * 8)
+    x = torch.empty((S, C), dtype=torch.complex64, device="cuda"); ppf.synth(C, S * C, seed=3, out=x)
+    y = torch.empty((S - T + 1, C), dtype=torch.complex64, device="cuda")
+    with ppf.Plan(C, T, ppf.generate_prototype(C, T)) as p:
+        t = timeit(lambda: p.fir(x, out=y))
+        te = timeit(lambda: p.fir_fft(x, out=y))
+    print(json.dumps({"T": T, "fir_frac": round(2 * S * C * 8 / t / 1e9 / peak, 3),
+                      "exact_fir_fft_frac": round(2 * S * C * 8 / te / 1e9 / peak, 3)}), flush=True)

@@ -33,7 +33,7 @@ def test_fir_golden_bitwise(cuda, golden):
 
 
 @pytest.mark.parametrize("C", [1, 2, 3, 8, 64, 100, 256, 1024, 4096])
-@pytest.mark.parametrize("T", [1, 2, 4, 7, 8, 16, 17, 20, 24, 32, 48, 64, 128])
+@pytest.mark.parametrize("T", [1, 2, 4, 7, 8, 12, 16, 17, 20, 24, 32, 48, 64, 128])
 def test_fir_bitwise_vs_oracle(cuda, port, C, T):
     ppf = ppf_mod()
     rng = np.random.default_rng(C * 1000 + T)
@@ -42,8 +42,12 @@ def test_fir_bitwise_vs_oracle(cuda, port, C, T):
     coeffs = port.generate_prototype(C, T, 9.0)
     with ppf.Plan(C, T, coeffs) as p:
         got = p.fir(x)
+    with ppf.Plan(C, T, coeffs, flags=ppf.K1_PREFETCH) as p:
+        got_prefetch = p.fir(x)
     assert got.shape == (S - T + 1, C)
-    assert np.array_equal(bits(got), bits(port.fir(x, C, T, coeffs)))
+    want = bits(port.fir(x, C, T, coeffs))
+    assert np.array_equal(bits(got), want)
+    assert np.array_equal(bits(got_prefetch), want)
 
 
 def test_fir_errors(cuda):
