@@ -131,7 +131,9 @@ template <int TC, int K, int LAG, int RB>
 struct FirTma {
     static constexpr int CPW = 32 / K;
     // rows a warp needs at once: the newest row of every tap chunk plus the
-    // window prefill, rounded to chunks, plus two chunks of lookahead
+    // window prefill, rounded to chunks, plus two chunks of lookahead (not
+    // rounded up to a power of two: at TC = 16 that would cost the second
+    // block per SM its shared memory)
     static constexpr int SPAN = TC - 1 + (K - 1) * (TC - LAG);
     static constexpr int NS = (SPAN + TC) / RB + 3;
     static constexpr size_t RING_FLOATS2 = size_t(NS) * RB * CPW;
@@ -254,6 +256,128 @@ __global__ void __launch_bounds__(256, MINB) fir_tma_kernel(const __grid_constan
             if (live && qq == K - 1 && tau < steps && s >= s0 && s < s1)
                 __stcs(out + s * C + c, make_float2(__double2float_rn(acc.x),
                                                     __double2float_rn(acc.y)));
+        }
+    }
+}
+
+// K1f — FIR in FP32 for PPFG_FAST's unfused path (T > 16, where no fused
+// kernel exists): K lanes per channel each own TC consecutive taps and
+// accumulate their partial sum with packed FFMA2 (re and im together); the K
+// partials are added in a fixed tree order with shuffles. Not bit-exact by
+// design (reassociated FP32 sum; max|err|/RMS ~1e-6, inside the FAST
+// tolerance); ppfg_fir itself always runs the exact K1/K1t. Input staged by
+// TMA in a per-warp ring as in K1t.
+template <int TC, int K, int RB>
+struct FirFast {
+    static_assert(TC % 2 == 0 && (K & (K - 1)) == 0, "even tap chunks, power-of-two lanes");
+    static constexpr int CPW = 32 / K;
+    static constexpr int SPAN = TC - 1 + (K - 1) * TC;
+    static constexpr int NS_MIN = (SPAN + TC) / RB + 3;
+    // a power of two, so slot and parity are masks and shifts
+    static constexpr int NS = NS_MIN <= 4 ? 4 : NS_MIN <= 8 ? 8 : NS_MIN <= 16 ? 16 : 32;
+    static constexpr size_t RING_FLOATS2 = size_t(NS) * RB * CPW;
+    static constexpr int WARPS = 8;
+    static constexpr size_t BAR_OFF = sizeof(float2) * RING_FLOATS2 * WARPS;
+    static constexpr size_t SMEM = BAR_OFF + sizeof(uint64_t) * NS * WARPS;
+};
+
+template <int TC, int K, int RB>
+__global__ void __launch_bounds__(256, 3) fir_fast_kernel(const __grid_constant__ CUtensorMap map,
+                                                          float2* __restrict__ out, unsigned C,
+                                                          long long S_out,
+                                                          const float* __restrict__ taps, int seg,
+                                                          long long n_tasks) {
+    using F = FirFast<TC, K, RB>;
+    constexpr int CPW = F::CPW, NS = F::NS;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    float2* ring = reinterpret_cast<float2*>(smem_raw) + warp * F::RING_FLOATS2;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + F::BAR_OFF) + warp * NS;
+    const long long task = static_cast<long long>(blockIdx.x) * F::WARPS + warp;
+    if (task >= n_tasks)
+        return;
+    const int q = lane / CPW;
+    const int cl = lane - q * CPW;
+    const long long n_cb = (C + CPW - 1) / CPW;
+    const long long sg = task / n_cb;
+    const unsigned c0 = static_cast<unsigned>((task - sg * n_cb) * CPW);
+    const unsigned c_raw = c0 + cl;
+    const bool live = q < K && c_raw < C;
+    const unsigned c = live ? c_raw : 0u;
+    const int qq = q < K ? q : K - 1;
+    const long long s0 = sg * seg;
+    const long long s1 = min(s0 + seg, S_out);
+    const int steps = static_cast<int>(s1 - s0);
+    const int n_rows = steps + F::SPAN;
+    const int n_chunks = (n_rows + RB - 1) / RB;
+
+    if (lane == 0) {
+        for (int i = 0; i < NS; ++i)
+            mbar_init(full + i, 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    auto issue = [&](int k) {
+        const int slot = k % NS;
+        mbar_arrive_expect_tx(full + slot, static_cast<uint32_t>(sizeof(float2) * RB * CPW));
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(ring + slot * RB * CPW)),
+            "l"(reinterpret_cast<uint64_t>(&map)), "r"(static_cast<int>(c0)),
+            "r"(static_cast<int>(s0 + static_cast<long long>(k) * RB)), "r"(smem_u32(full + slot))
+            : "memory");
+    };
+    if (lane == 0)
+        for (int k = 0; k < NS && k < n_chunks; ++k)
+            issue(k);
+    int waited = 0, released = 0;
+    auto wait_upto = [&](int rr) {
+        const int k1 = min(rr / RB, n_chunks - 1);
+        for (; waited <= k1; ++waited)
+            mbar_wait(full + waited % NS, static_cast<uint32_t>((waited / NS) & 1));
+    };
+    auto row = [&](int rr) { return ring[((rr / RB) % NS) * RB * CPW + (rr % RB) * CPW + cl]; };
+
+    float h[TC];
+#pragma unroll
+    for (int t = 0; t < TC; ++t)
+        h[t] = __ldg(taps + static_cast<size_t>(qq * TC + t) * C + c);
+    const int base = qq * TC; // lane q's rows for output s0+tau: base + tau + [0, TC)
+    wait_upto(F::SPAN - 1);
+    float2 w[TC];
+#pragma unroll
+    for (int t = 0; t + 1 < TC; ++t)
+        w[t] = row(base + t);
+    for (int tau0 = 0; tau0 < steps; tau0 += TC) {
+        const int done = (tau0 + TC - 1) / RB;
+        __syncwarp();
+        for (; released < done; ++released)
+            if (lane == 0 && released + NS < n_chunks)
+                issue(released + NS);
+        wait_upto(tau0 + TC - 1 + F::SPAN);
+#pragma unroll
+        for (int u = 0; u < TC; ++u) {
+            const int tau = tau0 + u;
+            w[(u + TC - 1) % TC] = row(base + tau + TC - 1);
+            // two interleaved partial sums (even / odd taps) halve the
+            // dependent FFMA2 chain
+            float2 acc = mul2s(h[0], w[u % TC]);
+            float2 acc1 = mul2s(h[1], w[(u + 1) % TC]);
+#pragma unroll
+            for (int t = 2; t < TC; t += 2) {
+                acc = fma2s(h[t], w[(u + t) % TC], acc);
+                acc1 = fma2s(h[t + 1], w[(u + t + 1) % TC], acc1);
+            }
+            acc = add2(acc, acc1);
+#pragma unroll
+            for (int off = (K / 2) * CPW; off >= CPW; off >>= 1) {
+                acc.x += __shfl_down_sync(0xffffffffu, acc.x, off);
+                acc.y += __shfl_down_sync(0xffffffffu, acc.y, off);
+            }
+            const long long s = s0 + tau;
+            if (live && q == 0 && tau < steps)
+                __stcs(out + s * C + c, acc);
         }
     }
 }

@@ -249,6 +249,21 @@ FirTmaEntry fir_tma_table(int T) {
     }
 }
 
+template <int TC, int K, int RB>
+FirTmaEntry fir_fast_entry() {
+    return {reinterpret_cast<KernelFn>(&fir_fast_kernel<TC, K, RB>), K, RB, FirFast<TC, K, RB>::SMEM};
+}
+
+// K1f shapes: FP32 FIR for PPFG_FAST where no fused kernel covers T
+FirTmaEntry fir_fast_table(int T) {
+    switch (T) {
+    case 32: return fir_fast_entry<16, 2, 8>();
+    case 64: return fir_fast_entry<16, 4, 8>();
+    case 128: return fir_fast_entry<16, 8, 8>();
+    default: return {};
+    }
+}
+
 FirEntry fir_table(int T) {
     switch (T) {
 #define PPFG_FIR(t, tc, k)                                                                        \
@@ -618,9 +633,45 @@ int launch_fused(ppfg_plan p, const float2* din, uint64_t S_in, float2* dout, cu
 // transforms them in place. (Chunking this into L2-resident pieces was
 // measured slower: per-chunk waves and launches cost more than the DRAM
 // round trip saves.)
+// K1f: FP32 FIR (PPFG_FAST only), TMA-staged; false if no kernel applies
+bool launch_fir_fast(ppfg_plan p, const float2* din, uint64_t S_in, float2* dout, cudaStream_t st,
+                     int* rc) {
+    const uint64_t C = p->C, T = p->T;
+    const FirTmaEntry et = fir_fast_table(static_cast<int>(T));
+    if (!et.fn || C % 2 || reinterpret_cast<uintptr_t>(din) % 16)
+        return false;
+    const uint64_t S_out = S_in - T + 1;
+    const uint64_t cpw = 32 / et.k;
+    const uint64_t n_cb = cdiv(C, cpw);
+    const uint64_t target_tasks = static_cast<uint64_t>(p->num_sms) * 16 * 4;
+    uint64_t seg = cdiv(S_out * n_cb, target_tasks);
+    seg = std::max<uint64_t>(seg, std::min<uint64_t>(std::max<uint64_t>(64, 2 * T), S_out));
+    long long n_tasks = static_cast<long long>(cdiv(S_out, seg) * n_cb);
+    int seg_i = static_cast<int>(seg);
+    unsigned Cu = static_cast<unsigned>(C);
+    long long S_out_ll = static_cast<long long>(S_out);
+    const unsigned blocks = static_cast<unsigned>(cdiv(static_cast<uint64_t>(n_tasks), 8));
+    CUtensorMap map;
+    *rc = encode_rows_map(&map, din, C, S_in, static_cast<int>(cpw), et.rb);
+    if (*rc == PPFG_OK)
+        *rc = ensure_smem_attr(et.fn, et.smem, p->device);
+    if (*rc != PPFG_OK)
+        return true;
+    void* args[] = {&map, &dout, &Cu, &S_out_ll, &p->d_taps, &seg_i, &n_tasks};
+    *rc = cudaLaunchKernel(et.fn, dim3(blocks), dim3(256), args, et.smem, st) == cudaSuccess
+              ? check_launch("fir kernel (FP32, FAST)")
+              : fail(PPFG_CUDA_ERROR, "fir kernel (FP32, FAST): launch failed");
+    return true;
+}
+
 int launch_fir_fft(ppfg_plan p, const float2* din, uint64_t S_in, float2* dout, cudaStream_t st) {
     if (p->fused && !(p->flags & PPFG_UNFUSED))
         return launch_fused(p, din, S_in, dout, st);
+    int rc = PPFG_OK;
+    if ((p->flags & PPFG_FAST) && launch_fir_fast(p, din, S_in, dout, st, &rc)) {
+        PPFG_TRY(rc);
+        return launch_channelize(p, dout, S_in - p->T + 1, dout, true, st);
+    }
     PPFG_TRY(launch_fir(p, din, S_in, dout, st, false));
     return launch_channelize(p, dout, S_in - p->T + 1, dout, true, st);
 }

@@ -30,7 +30,8 @@ def main():
     ppf.synth(C, S * C, seed=3, out=x)
     y = torch.empty((S - T + 1, C), dtype=torch.complex64, device=dev)
     flags = {"fast": ppf.FAST, "exact": ppf.EXACT, "unfused": ppf.UNFUSED,
-             "cluster": ppf.FAST | ppf.CLUSTER, "exact-cluster": ppf.CLUSTER}[a.mode]
+             "cluster": ppf.FAST | ppf.CLUSTER, "exact-cluster": ppf.CLUSTER,
+             "fast-unfused": ppf.FAST | ppf.UNFUSED}[a.mode]
     with ppf.Plan(C, T, ppf.generate_prototype(C, T), flags=flags) as p:
         for _ in range(a.reps):
             if a.op == "fir":
