@@ -68,6 +68,7 @@ struct FusedCfg {
     // unit per FFT thread per pass
     static constexpr int B = (NFFT << W) / (N * G) > 0 ? (NFFT << W) / (N * G) : 1;
     static constexpr int PC = PC_;          // ring chunks (of B input spectra) per group
+    static constexpr int FFT_WG = FFT_WG_;
     // batches per unrolled FIR loop body, so the window rotation is pure renaming
     static constexpr int BU = ilcm(B, T) / B;
     static constexpr unsigned STRIDE = sw_row_stride(N);
@@ -104,7 +105,17 @@ struct FusedRows {
     }
 };
 
-// named barriers: 0 = __syncthreads, FULL = 1+t, EMPTY = 3+t, FFT passes = 5
+// Tile row r of an FFT warpgroup that owns rows [off, off + rows): map its
+// local row index to the tile's output rows.
+struct OffsetRows {
+    FusedRows base;
+    int off;
+    PPFG_DEV long long operator()(int r) const { return base(r + off); }
+};
+
+// named barriers: 0 = __syncthreads, FULL = 1+t, EMPTY = 3+t, FFT passes =
+// 5 + warpgroup (rows are independent: each FFT warpgroup transforms its own
+// rows of the tile and syncs only with itself between passes)
 PPFG_DEV void named_sync(int id, int count) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
@@ -162,7 +173,13 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
         // ================================ FFT role ================================
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(Cfg::FFT_REGS));
         const int ftid = tid - NFIR;
-        using Passes = FftPasses<L, L - RLOG, Cfg::W, false, true, NFFT, 0, true, POWER>;
+        // per-warpgroup rows where the tile splits evenly, else CTA-wide passes
+        constexpr bool SPLIT = Cfg::TILE_ROWS % Cfg::FFT_WG == 0;
+        constexpr int PNT = SPLIT ? 128 : NFFT;                 // threads per pass group
+        constexpr int PROWS = SPLIT ? Cfg::TILE_ROWS / Cfg::FFT_WG : Cfg::TILE_ROWS;
+        const int pg = SPLIT ? ftid / 128 : 0;                  // pass group
+        const int ptid = ftid - pg * PNT;
+        using Passes = FftPasses<L, L - RLOG, Cfg::W, false, true, PNT, 0, true, POWER>;
         constexpr int EL = Passes::E_LAST;
         double pacc[POWER ? EL : 1];
 #pragma unroll
@@ -171,18 +188,19 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
         for (long long b = 0; b < n_batches; ++b) {
             const int t = static_cast<int>(b & 1);
             named_sync(1 + t, NT);
-            Passes::run(nullptr, out, tiles + t * Cfg::TILE_ROWS * Cfg::STRIDE, Cfg::STRIDE,
-                        static_cast<int>(Cfg::TILE_ROWS), FusedRows{o0, o1, rpg, b * B, B}, tw,
-                        ftid, SyncNamed{5, NFFT}, pacc);
+            Passes::run(nullptr, out,
+                        tiles + (t * Cfg::TILE_ROWS + pg * PROWS) * Cfg::STRIDE, Cfg::STRIDE,
+                        PROWS, OffsetRows{FusedRows{o0, o1, rpg, b * B, B}, pg * PROWS}, tw, ptid,
+                        SyncNamed{5 + pg, PNT}, pacc);
             named_arrive(3 + t, NT);
         }
         if constexpr (POWER) {
-            // the last pass gives thread ftid exactly one unit: tile row r,
+            // the last pass gives each thread exactly one unit: tile row r,
             // bins u + rev_L(k)
             constexpr int UL = N / EL;
-            static_assert(Cfg::TILE_ROWS * UL == NFFT, "one last-pass unit per FFT thread");
-            const int r = ftid / UL;
-            const unsigned u = static_cast<unsigned>(ftid % UL);
+            static_assert(PROWS * UL == PNT, "one last-pass unit per FFT thread");
+            const int r = pg * PROWS + ptid / UL;
+            const unsigned u = static_cast<unsigned>(ptid % UL);
             double* part = reinterpret_cast<double*>(out) +
                            (static_cast<size_t>(blockIdx.x) * Cfg::TILE_ROWS + r) * N + u;
 #pragma unroll
