@@ -202,6 +202,42 @@ def run_reference_arm(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def pcie_probe(hx, hy, dx, dy, n_bytes=1 << 30, reps=3):
+    """Raw pinned copy bandwidth of this box (GB/s, per direction): H2D alone,
+    D2H alone, and both at once — the ceiling the e2e number runs against."""
+    import torch
+
+    def raw(t):
+        return torch.view_as_real(t).reshape(-1).view(torch.uint8)
+
+    n = min(n_bytes, hx.numel() * 8, hy.numel() * 8, dx.numel() * 8, dy.numel() * 8)
+    hi, ho, di, do = raw(hx)[:n], raw(hy)[:n], raw(dx)[:n], raw(dy)[:n]
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def h2d():
+        with torch.cuda.stream(s1):
+            di.copy_(hi, non_blocking=True)
+
+    def d2h():
+        with torch.cuda.stream(s2):
+            ho.copy_(do, non_blocking=True)
+
+    def both():
+        h2d()
+        d2h()
+
+    out = {}
+    for name, fn in (("h2d", h2d), ("d2h", d2h), ("bidir_each_way", both)):
+        fn()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            fn()
+        torch.cuda.synchronize()
+        out[name] = n * reps / (time.perf_counter() - t0) / 1e9
+    return out
+
+
 def ncu_traffic(C, T, mode, n_spectra_in):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
     kernel, from the committed `ncu --set full` capture of this same
@@ -356,7 +392,8 @@ def main():
         e2e = {"value": in_all * args.e2e_steps / te_max / 1e9, "unit": "GB/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(oc * row_b),
                "steps": args.e2e_steps, "x_realtime": in_all * args.e2e_steps / te_max / SKA_RATE,
-               "path": "ppfg_fir_fft(mem=HOST), pinned buffers, 64 MiB double-buffered chunks"}
+               "path": "ppfg_fir_fft(mem=HOST), pinned buffers, 64 MiB double-buffered chunks",
+               "pcie_limit": pcie_probe(hx, hy, x, y)}
         del hx, hy
 
     # ---- CPU baseline: the reference on this host, N=1 rank 0 only ----

@@ -877,7 +877,10 @@ int run_host(ppfg_plan p, Op op, const void* hin, uint64_t n_in_rows, void* hout
         const int b = static_cast<int>(i & 1);
         const uint64_t o = i * chunk, n = std::min(chunk, n_out_rows - o);
         const uint64_t in_bytes = (n + halo) * row_bytes, out_bytes = n * row_bytes;
-        if (i >= 2)
+        // pageable outputs: copy chunk i-2 out of its staging buffer before
+        // reusing it (pinned outputs need no host sync: every reuse below is
+        // ordered on the device by events, so H2D, kernels and D2H overlap)
+        if (i >= 2 && !pin_out)
             PPFG_TRY(drain(i - 2));
         // input: d_in[b] is free once chunk i-2's kernel has run
         if (i >= 2)
@@ -904,8 +907,10 @@ int run_host(ppfg_plan p, Op op, const void* hin, uint64_t n_in_rows, void* hout
                                   p->d_out[b], out_bytes, cudaMemcpyDeviceToHost, p->s_d2h));
         PPFG_CUDA(cudaEventRecord(p->ev_d2h[b], p->s_d2h));
     }
-    for (uint64_t i = n_chunks >= 2 ? n_chunks - 2 : 0; i < n_chunks; ++i)
-        PPFG_TRY(drain(i));
+    if (!pin_out)
+        for (uint64_t i = n_chunks >= 2 ? n_chunks - 2 : 0; i < n_chunks; ++i)
+            PPFG_TRY(drain(i));
+    PPFG_CUDA(cudaStreamSynchronize(p->s_d2h));
     PPFG_CUDA(cudaStreamSynchronize(p->stream));
     return PPFG_OK;
 }
