@@ -237,14 +237,16 @@ FirTmaEntry fir_tma_entry() {
 }
 
 // K1t shapes (TMA-staged input; measured FIR-only at C = 1024: T = 8 0.87 vs
-// 0.79, T = 16 0.66 vs 0.50 of the HBM roofline). The lane-chained shapes
-// (T > 16) stay on the register-prefetch K1, which measured faster there.
+// 0.79, T = 16 0.66 vs 0.50, T = 32 (one lane per channel, 244 registers,
+// 8 warps/SM) 0.36 vs 0.23 of the HBM roofline). Lane-chained K1t variants
+// measured slower than the register-prefetch K1, which keeps the other T.
 FirTmaEntry fir_tma_table(int T) {
     switch (T) {
     case 4: return fir_tma_entry<4, 1, 8>();
     case 8: return fir_tma_entry<8, 1, 8>();
     case 12: return fir_tma_entry<12, 1, 8>();
     case 16: return fir_tma_entry<16, 1, 8>();
+    case 32: return fir_tma_entry<32, 1, 8, 1>();
     default: return {};
     }
 }
