@@ -587,8 +587,10 @@ int launch_channelize(ppfg_plan p, const float2* din, uint64_t rows, float2* dou
         return rc;
     }
     const int L = p->L;
-    if (p->fft_fused) // T = 1 fused kernel with unit taps (in place is safe: row s is
-                      // written only after it was read, and nothing else reads it)
+    // T = 1 fused kernel with unit taps (in place is safe: row s is written
+    // only after it was read, and nothing else reads it); TMA needs a
+    // 16-byte-aligned source
+    if (p->fft_fused && reinterpret_cast<uintptr_t>(din) % 16 == 0)
         return launch_fused_entry(p, p->fft_fused, p->d_ones, 1, din, rows, dout, st);
     if (const FftEntry* e = fft_table(L)) {
         PPFG_TRY(ensure_smem_attr(e->fn, e->smem, p->device));
@@ -666,8 +668,13 @@ bool launch_fir_fast(ppfg_plan p, const float2* din, uint64_t S_in, float2* dout
     return true;
 }
 
+// TMA (bulk and tensor copies) reads need a 16-byte-aligned source; a caller's
+// buffer that is only 8-byte aligned (e.g. a view starting at an odd sample)
+// takes the plain-load kernels instead
+bool aligned16(const void* ptr) { return reinterpret_cast<uintptr_t>(ptr) % 16 == 0; }
+
 int launch_fir_fft(ppfg_plan p, const float2* din, uint64_t S_in, float2* dout, cudaStream_t st) {
-    if (p->fused && !(p->flags & PPFG_UNFUSED))
+    if (p->fused && !(p->flags & PPFG_UNFUSED) && aligned16(din))
         return launch_fused(p, din, S_in, dout, st);
     int rc = PPFG_OK;
     if ((p->flags & PPFG_FAST) && launch_fir_fast(p, din, S_in, dout, st, &rc)) {
@@ -721,7 +728,7 @@ int launch_fir_fft_mean_power(ppfg_plan p, const float2* din, uint64_t S_in, dou
                               cudaStream_t st) {
     const uint64_t S_out = S_in - p->T + 1;
     const FusedEntry* e = p->fused;
-    if (e && e->power_fn && !(p->flags & PPFG_UNFUSED)) {
+    if (e && e->power_fn && !(p->flags & PPFG_UNFUSED) && aligned16(din)) {
         PPFG_TRY(ensure_smem_attr(e->power_fn, e->smem, p->device));
         const uint64_t grid =
             std::max<uint64_t>(1, std::min<uint64_t>(p->num_sms, cdiv(S_out, e->rows_per_batch)));

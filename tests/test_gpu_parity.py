@@ -381,3 +381,34 @@ def test_fir_fft_mean_power(cuda, port, C, T, flags):
         assert _rel(fused, want) <= 1e-13              # bins bit-exact: only the sum order differs
     else:
         assert _rel(fused, want) <= 2e-5 * np.log2(C)  # FP32 FIR: |X|^2 inherits 2x its error
+
+
+@pytest.mark.parametrize("C,T,flags", [(1024, 8, "fast"), (512, 8, "exact"), (2048, 8, "fast"),
+                                       (1024, 16, "exact"), (1024, 4, "exact")])
+def test_misaligned_device_views(cuda, port, C, T, flags):
+    """Buffers that start 8 bytes past a 16-byte boundary (a view at an odd
+    sample) cannot feed TMA: the plain-load kernels must take them, same results."""
+    import torch
+    ppf = ppf_mod()
+    S = T - 1 + 300
+    x = ppf.synth(C, S * C, seed=C + T)
+    coeffs = port.generate_prototype(C, T, 9.0)
+    want = port.fir_fft(x, C, T, coeffs).view(np.complex64)
+    buf = torch.zeros(S * C + 1, dtype=torch.complex64, device=cuda)
+    view = buf[1:]
+    view.copy_(torch.from_numpy(x.reshape(-1)))
+    assert view.data_ptr() % 16 == 8
+    f = ppf.FAST if flags == "fast" else ppf.EXACT
+    with ppf.Plan(C, T, coeffs, flags=f) as p:
+        got = p.fir_fft(view).cpu().numpy()
+        fir = p.fir(view).cpu().numpy()
+        mp = p.fir_fft_mean_power(view)
+        chan = p.channelize(view).cpu().numpy()
+    torch.cuda.synchronize()
+    if flags == "exact":
+        assert np.array_equal(bits(got), bits(want))
+    else:
+        assert max_err_over_rms(got, want) <= 1e-5 * np.log2(C)
+    assert np.array_equal(bits(fir), bits(port.fir(x, C, T, coeffs)))
+    assert np.array_equal(bits(chan), bits(port.channelize(x, C)))
+    assert _rel(mp.cpu().numpy(), port.mean_power(port.fir_fft(x, C, T, coeffs), C)) <= 2e-5 * np.log2(C)
