@@ -151,7 +151,8 @@ const std::vector<FusedEntry>& fused_table() {
         fused_entry<FusedCfg<6, 8, 1, true>>(),
         fused_entry<FusedCfg<10, 4, 2, true>>(),
         // T = 1 with unit taps: x*1 == x exactly, so these are bit-exact,
-        // TMA-fed, warp-specialised FFTs — channelize_block for 64 <= C <= 2048
+        // TMA-fed, warp-specialised FFTs — channelize_block for 64 <= C <= 4096
+        // (C = 4096: 0.76 of roofline vs 0.69 for K2)
         // (split-kernel T = 1 entries for C = 4096, 8192 and FP64 C = 4096 on
         // 8-CTA clusters measured slower than K2 / the unfused path)
         fused_entry<FusedCfg<6, 1, 0, false, 120, 80, 2, 3>>(),
@@ -160,6 +161,7 @@ const std::vector<FusedEntry>& fused_table() {
         fused_entry<FusedCfg<9, 1, 1, false>>(),
         fused_entry<FusedCfg<10, 1, 2, false>>(),
         fused_entry<FusedCfg<11, 1, 3, false, 160, 96, 3>>(),
+        fused_entry<FusedCfg<12, 1, 4, false, 160, 96, 2>>(),
         // thread-block clusters, FIR split by channel block and FFT by
         // spectrum (fused_split.cuh) — for FIR state that does not fit one SM.
         // preferred = taken by default: measured faster than FIR -> HBM -> FFT
