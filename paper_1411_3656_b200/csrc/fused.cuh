@@ -50,8 +50,9 @@ constexpr int ilcm(int a, int b) {
 }
 
 template <int L_, int T_, int RLOG_, bool EXACT_, int FIR_REGS_ = 160, int FFT_REGS_ = 96,
-          int PC_ = 4, int FFT_WG_ = 2>
+          int PC_ = 4, int FFT_WG_ = 2, int NTILE_ = 2>
 struct FusedCfg {
+    static constexpr int NTILE = NTILE_; // FFT tiles in flight between the roles
     static constexpr int L = L_, T = T_, RLOG = RLOG_;
     static constexpr bool EXACT = EXACT_;
     static constexpr int FIR_REGS = FIR_REGS_, FFT_REGS = FFT_REGS_;
@@ -80,7 +81,7 @@ struct FusedCfg {
     static constexpr size_t TILE_OFF = RING_OFF + RING_BYTES;
     static constexpr size_t TILE_ROWS = size_t(G) * B;
     static constexpr size_t TILE_BYTES = sizeof(float2) * TILE_ROWS * STRIDE;
-    static constexpr size_t BAR_OFF = (TILE_OFF + 2 * TILE_BYTES + 7) & ~size_t(7);
+    static constexpr size_t BAR_OFF = (TILE_OFF + NTILE * TILE_BYTES + 7) & ~size_t(7);
     static constexpr size_t SMEM = BAR_OFF + sizeof(uint64_t) * 2 * G * PC;
     static_assert(NTG >= 32 && NTG <= NFIR && NFIR % NTG == 0, "FIR groups must be whole warps");
     // setmaxnreg moves registers within the CTA's launch allocation only: the
@@ -113,9 +114,10 @@ struct OffsetRows {
     PPFG_DEV long long operator()(int r) const { return base(r + off); }
 };
 
-// named barriers: 0 = __syncthreads, FULL = 1+t, EMPTY = 3+t, FFT passes =
-// 5 + warpgroup (rows are independent: each FFT warpgroup transforms its own
-// rows of the tile and syncs only with itself between passes)
+// named barriers: 0 = __syncthreads, FULL = 1+t, EMPTY = 1+NTILE+t, FFT
+// passes = 1+2*NTILE + warpgroup (rows are independent: each FFT warpgroup
+// transforms its own rows of the tile and syncs only with itself between
+// passes)
 PPFG_DEV void named_sync(int id, int count) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
@@ -186,13 +188,13 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
         for (int k = 0; k < (POWER ? EL : 1); ++k)
             pacc[k] = 0.0;
         for (long long b = 0; b < n_batches; ++b) {
-            const int t = static_cast<int>(b & 1);
+            const int t = static_cast<int>(b % Cfg::NTILE);
             named_sync(1 + t, NT);
             Passes::run(nullptr, out,
                         tiles + (t * Cfg::TILE_ROWS + pg * PROWS) * Cfg::STRIDE, Cfg::STRIDE,
                         PROWS, OffsetRows{FusedRows{o0, o1, rpg, b * B, B}, pg * PROWS}, tw, ptid,
-                        SyncNamed{5 + pg, PNT}, pacc);
-            named_arrive(3 + t, NT);
+                        SyncNamed{1 + 2 * Cfg::NTILE + pg, PNT}, pacc);
+            named_arrive(1 + Cfg::NTILE + t, NT);
         }
         if constexpr (POWER) {
             // the last pass gives each thread exactly one unit: tile row r,
@@ -269,7 +271,7 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
 #pragma unroll
         for (int u = 0; u < BU; ++u) {
             const long long b = b0 + u;
-            const int t = static_cast<int>(b & 1);
+            const int t = static_cast<int>(b % Cfg::NTILE);
             const int slot = static_cast<int>(b % PC);
             const bool have = b < n_chunks;
             if (producer && b >= 1 && b - 1 + PC < n_chunks) {
@@ -278,8 +280,8 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
                 fence_proxy_async();
                 issue(b - 1 + PC);
             }
-            if (b >= 2)
-                named_sync(3 + t, NT); // the FFT role has drained tile t
+            if (b >= Cfg::NTILE)
+                named_sync(1 + Cfg::NTILE + t, NT); // the FFT role has drained tile t
             if (have)
                 mbar_wait(full_g + slot, static_cast<uint32_t>((b / PC) & 1));
             const float2* chunk = ring_g + static_cast<size_t>(slot) * B * N + j;
