@@ -67,8 +67,10 @@ enum {
     PPFG_FAST = 1u,
     PPFG_UNFUSED = 2u,
     PPFG_CLUSTER = 4u,
-    PPFG_K1_PREFETCH = 8u /* comparison only: FIR-only kernel with register prefetch
-                             instead of TMA-staged input (same results) */
+    PPFG_K1_PREFETCH = 8u, /* comparison only: FIR-only kernel with register prefetch
+                              instead of TMA-staged input (same results) */
+    PPFG_FIR_LEGACY = 16u  /* comparison only: the lane-window FIR kernels (K1/K1t/K1f)
+                              instead of the register-blocked K1b for T >= 16 */
 };
 
 typedef struct ppfg_plan_s* ppfg_plan;

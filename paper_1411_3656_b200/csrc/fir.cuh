@@ -21,6 +21,8 @@
 
 #include <cuda.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace ppfg {
@@ -409,6 +411,145 @@ __global__ void __launch_bounds__(256) fir_exact_generic_kernel(const float2* __
             ai = __fma_rn(ht, static_cast<double>(x.y), ai);
         }
         out[s * C + c] = make_float2(__double2float_rn(ar), __double2float_rn(ai));
+    }
+}
+
+
+// K1b — register-blocked FIR for long filters (T >= 16), exact (FP64, the
+// reference's per-output op sequence) or FP32 (PPFG_FAST). A CTA of NW warps
+// owns 32 consecutive channels (lane = channel) of one time segment and
+// streams its input rows through a CTA-wide shared-memory ring of chunks of
+// RB = NW*U rows (one 2-D TMA tensor copy each, SASS UTMALDG). Per step,
+// warp w computes the U consecutive outputs [k*RB + w*U, +U) of its lane's
+// channel: it reads each of the U+T-1 input rows it needs ONCE from shared
+// memory and applies it to all U accumulators that use it (output u takes row
+// j with tap j-u), taps held in registers. So an input row costs one LDS.64
+// per U outputs' worth of taps — no register window rotation and no lane
+// shuffles (K1's chain and K1f's tree) — and each output still accumulates
+// its taps in ascending order: acc = fma(h_0, x_0, init) then fma(h_t, x_t,
+// acc), i.e. bit-identical to ppf_fir_optimized (fir.hpp:85-110) in the
+// exact mode. The FP32 mode runs the same chain in packed FFMA2 (re and im
+// of one sample with the tap as a broadcast operand).
+template <int T, int U, int NW, bool EXACT>
+struct FirBlk {
+    static constexpr int NT = NW * 32;
+    static constexpr int RB = NW * U;                        // rows per chunk = per step
+    static constexpr int NEED = 1 + (T - 1 + RB - 1) / RB;   // chunks one step reads
+    static constexpr int NS_MIN = NEED + 2;                  // + two chunks of lookahead
+    static constexpr int NS = NS_MIN <= 4 ? 4 : NS_MIN <= 8 ? 8 : 16;
+    static constexpr int NR = NS * RB;                       // ring rows (power of two)
+    static constexpr size_t CHUNK_BYTES = sizeof(float2) * RB * 32;
+    static constexpr size_t BAR_OFF = sizeof(float2) * size_t(NR) * 32;
+    static constexpr size_t SMEM = BAR_OFF + sizeof(uint64_t) * NS;
+    static_assert((RB & (RB - 1)) == 0 && RB <= 256, "power-of-two chunks within a TMA box");
+};
+
+template <int T, int U, int NW, bool EXACT, int MINB>
+__global__ void __launch_bounds__(NW * 32, MINB) fir_block_kernel(const __grid_constant__ CUtensorMap map,
+                                                                  float2* __restrict__ out, unsigned C,
+                                                                  long long S_out,
+                                                                  const float* __restrict__ taps,
+                                                                  int seg, double init) {
+    using F = FirBlk<T, U, NW, EXACT>;
+    constexpr int RB = F::RB, NS = F::NS, NR = F::NR, NEED = F::NEED;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    float2* ring = reinterpret_cast<float2*>(smem_raw);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + F::BAR_OFF);
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const long long n_cb = (C + 31) / 32;
+    const long long sg = blockIdx.x / n_cb;
+    const unsigned c0 = static_cast<unsigned>((blockIdx.x - sg * n_cb) * 32);
+    const bool live = c0 + lane < C;
+    const unsigned c = live ? c0 + lane : C - 1;
+    const long long s0 = sg * seg;
+    const int rows = static_cast<int>(min(s0 + seg, S_out) - s0);
+    const int n_steps = (rows + RB - 1) / RB;
+    // chunks holding rows [0, rows + T - 1) (TMA zero-fills past the input)
+    const int n_chunks = (rows + T - 1 + RB - 1) / RB;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NS; ++i)
+            mbar_init(full + i, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    auto issue = [&](int k) { // thread 0 only
+        const int slot = k & (NS - 1);
+        mbar_arrive_expect_tx(full + slot, static_cast<uint32_t>(F::CHUNK_BYTES));
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(ring + slot * RB * 32)),
+            "l"(reinterpret_cast<uint64_t>(&map)), "r"(static_cast<int>(c0)),
+            "r"(static_cast<int>(s0 + static_cast<long long>(k) * RB)), "r"(smem_u32(full + slot))
+            : "memory");
+    };
+    if (threadIdx.x == 0)
+        for (int k = 0; k < NS && k < n_chunks; ++k)
+            issue(k);
+
+    using acc_t = typename std::conditional<EXACT, double2, float2>::type;
+    using tap_t = typename std::conditional<EXACT, double, float>::type;
+    tap_t h[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t)
+        h[t] = static_cast<tap_t>(__ldg(taps + static_cast<size_t>(t) * C + c));
+
+    int waited = 0;
+    for (int k = 0; k < n_steps; ++k) {
+        if (k > 0) {
+            // every warp is done with step k-1, the last reader of chunk k-1
+            __syncthreads();
+            if (threadIdx.x == 0 && k - 1 + NS < n_chunks)
+                issue(k - 1 + NS);
+        }
+        const int need = min(k + NEED - 1, n_chunks - 1);
+        for (; waited <= need; ++waited)
+            mbar_wait(full + (waited & (NS - 1)), static_cast<uint32_t>((waited / NS) & 1));
+
+        const int r0 = k * RB + warp * U;
+        // byte offset of (row r0, this lane) in the ring; rows wrap modulo NR
+        const uint32_t base = smem_u32(ring);
+        const uint32_t off0 = static_cast<uint32_t>(r0) * 256u + static_cast<uint32_t>(lane) * 8u;
+        acc_t acc[U];
+#pragma unroll
+        for (int j = 0; j < U + T - 1; ++j) {
+            const uint32_t off = (off0 + static_cast<uint32_t>(j) * 256u) & (uint32_t(NR) * 256u - 1u);
+            float2 x;
+            asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(x.x), "=f"(x.y) : "r"(base + off));
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int t = j - u;
+                if (t < 0 || t >= T)
+                    continue;
+                if constexpr (EXACT) {
+                    const double xr = static_cast<double>(x.x), xi = static_cast<double>(x.y);
+                    if (t == 0) {
+                        acc[u].x = __fma_rn(h[0], xr, init);
+                        acc[u].y = __fma_rn(h[0], xi, init);
+                    } else {
+                        acc[u].x = __fma_rn(h[t], xr, acc[u].x);
+                        acc[u].y = __fma_rn(h[t], xi, acc[u].y);
+                    }
+                } else {
+                    if (t == 0)
+                        acc[u] = mul2s(h[0], x);
+                    else
+                        acc[u] = fma2s(h[t], x, acc[u]);
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (live && r0 + u < rows) {
+                float2 y;
+                if constexpr (EXACT)
+                    y = make_float2(__double2float_rn(acc[u].x), __double2float_rn(acc[u].y));
+                else
+                    y = acc[u];
+                __stcs(out + (s0 + r0 + u) * C + c, y);
+            }
+        }
     }
 }
 

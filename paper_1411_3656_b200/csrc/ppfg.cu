@@ -268,6 +268,38 @@ FirTmaEntry fir_fast_table(int T) {
     }
 }
 
+// K1b shapes (register-blocked, CTA-wide TMA ring; fir.cuh): U = 16 outputs
+// per thread, 4 warps per CTA
+struct FirBlkEntry {
+    KernelFn fn = nullptr;
+    int rb = 0, nt = 0;
+    size_t smem = 0;
+};
+
+template <int T, int U, int NW, bool EXACT, int MINB>
+FirBlkEntry fir_blk_entry() {
+    using F = FirBlk<T, U, NW, EXACT>;
+    return {reinterpret_cast<KernelFn>(&fir_block_kernel<T, U, NW, EXACT, MINB>), F::RB, F::NT,
+            F::SMEM};
+}
+
+FirBlkEntry fir_blk_table(int T, bool exact) {
+    if (exact) {
+        switch (T) {
+        case 16: return fir_blk_entry<16, 16, 4, true, 3>();
+        case 32: return fir_blk_entry<32, 16, 4, true, 3>();
+        case 64: return fir_blk_entry<64, 16, 4, true, 2>();
+        default: return {};
+        }
+    }
+    switch (T) {
+    case 32: return fir_blk_entry<32, 16, 4, false, 3>();
+    case 64: return fir_blk_entry<64, 16, 4, false, 3>();
+    case 128: return fir_blk_entry<128, 16, 2, false, 3>();
+    default: return {};
+    }
+}
+
 FirEntry fir_table(int T) {
     switch (T) {
 #define PPFG_FIR(t, tc, k)                                                                        \
@@ -371,6 +403,54 @@ int stream_of(ppfg_plan p, void* s, cudaStream_t* out) {
 // ---------------------------------------------------------- launchers (device)
 int encode_rows_map(CUtensorMap* map, const float2* din, uint64_t C, uint64_t S_in, int cpw, int rb);
 
+// K1b launch: one CTA per (32-channel block, time segment); segments sized
+// so the grid is a whole number of co-resident waves and the (T-1)-row halo
+// each segment re-reads stays small. false if no K1b shape applies.
+bool launch_fir_block(ppfg_plan p, const float2* din, uint64_t S_in, float2* dout, cudaStream_t st,
+                      bool exact, double init, int* rc) {
+    const uint64_t C = p->C, T = p->T;
+    if ((p->flags & (PPFG_FIR_LEGACY | PPFG_K1_PREFETCH)) || C % 2 || reinterpret_cast<uintptr_t>(din) % 16)
+        return false;
+    const FirBlkEntry e = fir_blk_table(static_cast<int>(T), exact);
+    if (!e.fn)
+        return false;
+    *rc = ensure_smem_attr(e.fn, e.smem, p->device);
+    if (*rc != PPFG_OK)
+        return true;
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, e.fn, e.nt, e.smem);
+    per_sm = std::max(per_sm, 1);
+    const uint64_t S_out = S_in - T + 1;
+    const uint64_t n_cb = cdiv(C, 32);
+    const uint64_t slots = static_cast<uint64_t>(p->num_sms) * per_sm;
+    const uint64_t min_seg = std::min<uint64_t>(std::max<uint64_t>(32 * T, 4 * e.rb), S_out);
+    uint64_t n_seg = 1;
+    for (uint64_t waves = 8; waves >= 1; waves /= 2) {
+        const uint64_t ns = std::max<uint64_t>(1, waves * slots / n_cb);
+        if (cdiv(S_out, ns) >= min_seg || waves == 1) {
+            n_seg = ns;
+            break;
+        }
+    }
+    uint64_t seg = cdiv(S_out, n_seg);
+    seg = std::max<uint64_t>(seg, min_seg);
+    seg = cdiv(seg, static_cast<uint64_t>(e.rb)) * e.rb; // whole steps
+    n_seg = cdiv(S_out, seg);
+    CUtensorMap map;
+    *rc = encode_rows_map(&map, din, C, S_in, 32, e.rb);
+    if (*rc != PPFG_OK)
+        return true;
+    unsigned Cu = static_cast<unsigned>(C);
+    long long S_out_ll = static_cast<long long>(S_out);
+    int seg_i = static_cast<int>(seg);
+    void* args[] = {&map, &dout, &Cu, &S_out_ll, &p->d_taps, &seg_i, &init};
+    *rc = cudaLaunchKernel(e.fn, dim3(static_cast<unsigned>(n_seg * n_cb)), dim3(e.nt), args, e.smem,
+                           st) == cudaSuccess
+              ? check_launch(exact ? "fir kernel (register-blocked)" : "fir kernel (register-blocked, FP32)")
+              : fail(PPFG_CUDA_ERROR, "fir kernel (register-blocked): launch failed");
+    return true;
+}
+
 int launch_fir(ppfg_plan p, const float2* din, uint64_t S_in, float2* dout, cudaStream_t st,
                bool reference_order) {
     const uint64_t T = p->T, C = p->C;
@@ -378,6 +458,9 @@ int launch_fir(ppfg_plan p, const float2* din, uint64_t S_in, float2* dout, cuda
     const double init = reference_order ? 0.0 : -0.0;
     long long S_in_ll = static_cast<long long>(S_in), S_out_ll = static_cast<long long>(S_out);
     unsigned Cu = static_cast<unsigned>(C);
+    int rc_blk = PPFG_OK;
+    if (launch_fir_block(p, din, S_in, dout, st, true, init, &rc_blk))
+        return rc_blk;
     // TMA needs 16-byte-aligned rows (even C) and base address
     const bool tma_ok = !(p->flags & PPFG_K1_PREFETCH) && (C % 2 == 0) &&
                         (reinterpret_cast<uintptr_t>(din) % 16 == 0);
@@ -643,6 +726,8 @@ int launch_fused(ppfg_plan p, const float2* din, uint64_t S_in, float2* dout, cu
 bool launch_fir_fast(ppfg_plan p, const float2* din, uint64_t S_in, float2* dout, cudaStream_t st,
                      int* rc) {
     const uint64_t C = p->C, T = p->T;
+    if (launch_fir_block(p, din, S_in, dout, st, false, -0.0, rc))
+        return true;
     const FirTmaEntry et = fir_fast_table(static_cast<int>(T));
     if (!et.fn || C % 2 || reinterpret_cast<uintptr_t>(din) % 16)
         return false;

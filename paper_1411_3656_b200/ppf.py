@@ -21,6 +21,7 @@ FAST = 1
 UNFUSED = 2
 CLUSTER = 4
 K1_PREFETCH = 8  # comparison only: register-prefetch FIR kernel
+FIR_LEGACY = 16  # comparison only: lane-window FIR kernels instead of K1b
 MEM_HOST = 0
 MEM_DEVICE = 1
 

@@ -50,6 +50,42 @@ def test_fir_bitwise_vs_oracle(cuda, port, C, T):
     assert np.array_equal(bits(got_prefetch), want)
 
 
+# K1b (register-blocked FIR, T >= 16): long enough streams for many steps,
+# several time segments and ring wrap-arounds, ragged channel counts (partial
+# 32-channel blocks), both operation orders; bitwise against the oracle and
+# against the lane-window kernels it replaces.
+@pytest.mark.parametrize("C,T,S", [(1024, 16, 9000), (1024, 32, 9000), (1024, 64, 9000),
+                                   (66, 32, 40000), (1000, 64, 5000), (2, 16, 70000),
+                                   (4096, 32, 1500), (128, 64, 64), (96, 16, 16)])
+def test_fir_block_bitwise(cuda, port, C, T, S):
+    ppf = ppf_mod()
+    x = ppf.synth(C, S * C, seed=C + 7 * T)
+    coeffs = port.generate_prototype(C, T, 9.0)
+    with ppf.Plan(C, T, coeffs) as p:
+        got = p.fir(x)
+        got_ref = p.fir_reference(x)
+    with ppf.Plan(C, T, coeffs, flags=ppf.FIR_LEGACY) as p:
+        legacy = p.fir(x)
+    want = bits(port.fir(x, C, T, coeffs))
+    assert np.array_equal(bits(got), want)
+    assert np.array_equal(bits(legacy), want)
+    assert np.array_equal(bits(got_ref), bits(port.fir(x, C, T, coeffs, reference_order=True)))
+
+
+# K1b in FP32 (PPFG_FAST unfused path, T = 32..128): FIR+FFT within the
+# north-star bound, and the FP32 FIR alone close to the exact one.
+@pytest.mark.parametrize("C,T,S", [(1024, 32, 6000), (1024, 64, 6000), (1024, 128, 3000),
+                                   (2048, 64, 1200), (66, 64, 9000)])
+def test_fir_block_fast(cuda, port, C, T, S):
+    ppf = ppf_mod()
+    x = ppf.synth(C, S * C, seed=C * 3 + T)
+    coeffs = port.generate_prototype(C, T, 9.0)
+    with ppf.Plan(C, T, coeffs, flags=ppf.FAST | ppf.UNFUSED) as p:
+        got = p.fir_fft(x)
+    want = port.fir_fft(x, C, T, coeffs).view(np.complex64)   # dft_naive for C = 66
+    assert max_err_over_rms(got, want) <= 1e-5 * np.log2(C)
+
+
 def test_fir_errors(cuda):
     ppf = ppf_mod()
     rng = np.random.default_rng(113)
