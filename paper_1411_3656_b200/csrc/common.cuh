@@ -88,6 +88,16 @@ PPFG_DEV float2 mul2s(float s, float2 b) { return mul2(make_float2(s, s), b); }
 //   t = br * (wr, wi) + m         -> (fma(br,wr,-(bi*wi)), fma(br,wi,bi*wr))
 //   hi = lo - t; lo = lo + t
 // 4 packed instructions (FMUL2, FFMA2, 2x FADD2) for the reference's 8.
+// Twiddles live in memory as float2 (wr, wi) — the reference's f32 table
+// entry — and are expanded in registers to the (wr, wi, -wi, wr) operand
+// bfly2 consumes: one MOV and one sign-bit LOP3 (exact negation) per twiddle,
+// off the FMA pipe, for half the shared-memory bytes of a stored float4.
+PPFG_DEV float4 tw_expand(float2 w) {
+    uint32_t nwi;
+    asm("xor.b32 %0, %1, 0x80000000;" : "=r"(nwi) : "r"(__float_as_uint(w.y)));
+    return make_float4(w.x, w.y, __uint_as_float(nwi), w.x);
+}
+
 PPFG_DEV void bfly2(float2& lo, float2& hi, const float4 w) {
     const float2 m = mul2s(hi.y, make_float2(w.z, w.w));
     const float2 t = fma2s(hi.x, make_float2(w.x, w.y), m);

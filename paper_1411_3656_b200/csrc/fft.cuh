@@ -25,9 +25,18 @@
 
 namespace ppfg {
 
-// Twiddles are stored as float4 (wr, wi, -wi, wr) — the reference's f32 table
-// entry tw[h-1+j] (dft.hpp:93-96) plus the swizzled copy the packed butterfly
-// (bfly2) consumes.
+// Twiddles are stored either as float2 (wr, wi) — the reference's f32 table
+// entry tw[h-1+j] (dft.hpp:93-96) — expanded to the packed butterfly's
+// operand after the load (common.cuh tw_expand), or pre-expanded as float4
+// (wr, wi, -wi, wr): half the shared-memory bytes vs two fewer instructions
+// per twiddle, chosen per kernel by measurement.
+template <bool TW_SMEM>
+PPFG_DEV float4 tw_load(const float2* p) {
+    if constexpr (TW_SMEM)
+        return tw_expand(*p);
+    else
+        return tw_expand(__ldg(p));
+}
 template <bool TW_SMEM>
 PPFG_DEV float4 tw_load(const float4* p) {
     if constexpr (TW_SMEM)
@@ -37,15 +46,15 @@ PPFG_DEV float4 tw_load(const float4* p) {
 }
 
 // Stages for label bits [LO, LO+W), high bit first. v[k] has label fixed|k<<LO.
-template <int L, int LO, int W, bool TW_SMEM>
-PPFG_DEV void fft_stages(float2 (&v)[1 << W], unsigned fixed, const float4* __restrict__ tw) {
+template <int L, int LO, int W, bool TW_SMEM, class TW>
+PPFG_DEV void fft_stages(float2 (&v)[1 << W], unsigned fixed, const TW* __restrict__ tw) {
 #pragma unroll
     for (int bb = W - 1; bb >= 0; --bb) {
         const int b = LO + bb;
         const int s = L - b;
         const unsigned half = 1u << (s - 1);
         const unsigned jf = (s > 1) ? (__brev(fixed >> (b + 1)) >> (33 - s)) : 0u;
-        const float4* twb = tw + (half - 1) + jf;
+        const TW* twb = tw + (half - 1) + jf;
 #pragma unroll
         for (int k = 0; k < (1 << W); ++k) {
             if (k & (1 << bb))
@@ -99,10 +108,10 @@ struct FftSchedule {
 // accumulators pacc[k] — the caller guarantees one unit per thread, so
 // pacc[k] always belongs to the same tile row and bin.
 template <int L, int LO, int W, bool FIRST_GLOBAL, bool FINAL, bool TW_SMEM, int NT, bool POWER = false,
-          class RowMap>
+          class RowMap, class TW>
 PPFG_DEV void fft_tile_pass(const float2* gin, float2* gout,
                             float2* __restrict__ tile, unsigned row_stride, int rows,
-                            const RowMap& map, const float4* __restrict__ tw, int tid,
+                            const RowMap& map, const TW* __restrict__ tw, int tid,
                             double* pacc = nullptr) {
     constexpr int N = 1 << L;
     constexpr int E = 1 << W;
@@ -180,9 +189,9 @@ struct FftPasses {
     static constexpr int LO = S::lo(I);
     static constexpr bool LAST = (I == S::NP - 1);
     static constexpr int E_LAST = 1 << S::width(S::NP - 1); // values per unit in the last pass
-    template <class RowMap, class Sync>
+    template <class RowMap, class Sync, class TW>
     PPFG_DEV static void run(const float2* gin, float2* gout, float2* tile, unsigned row_stride,
-                             int rows, const RowMap& map, const float4* tw, int tid,
+                             int rows, const RowMap& map, const TW* tw, int tid,
                              const Sync& sync, double* pacc = nullptr) {
         fft_tile_pass<L, LO, WI, FIRST_GLOBAL && I == 0, LAST && STORE_LAST, TW_SMEM, NT,
                       LAST && POWER>(gin, gout, tile, row_stride, rows, map, tw, tid, pacc);
@@ -210,18 +219,18 @@ struct LinearRows {
 template <int L, int W, bool TW_SMEM, int NT>
 __global__ void __launch_bounds__(NT) fft_rows_kernel(const float2* in, float2* out,
                                                       long long n_rows,
-                                                      const float4* __restrict__ tw_g) {
+                                                      const float2* __restrict__ tw_g) {
     constexpr int N = 1 << L;
     constexpr int RB = (NT << W) / N > 0 ? (NT << W) / N : 1;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    float4* tw_s = reinterpret_cast<float4*>(smem_raw);
-    float2* tile = reinterpret_cast<float2*>(smem_raw + (TW_SMEM ? sizeof(float4) * N : 0));
+    float2* tw_s = reinterpret_cast<float2*>(smem_raw);
+    float2* tile = reinterpret_cast<float2*>(smem_raw + (TW_SMEM ? sizeof(float2) * N : 0));
     if constexpr (TW_SMEM) {
         for (int i = threadIdx.x; i < N - 1; i += NT)
             tw_s[i] = tw_g[i];
         __syncthreads();
     }
-    const float4* tw = TW_SMEM ? tw_s : tw_g;
+    const float2* tw = TW_SMEM ? tw_s : tw_g;
     constexpr unsigned stride = sw_row_stride(N);
     for (long long row0 = static_cast<long long>(blockIdx.x) * RB; row0 < n_rows;
          row0 += static_cast<long long>(gridDim.x) * RB) {
@@ -237,7 +246,7 @@ constexpr size_t fft_rows_smem_bytes() {
     constexpr int N = 1 << L;
     constexpr int RB = (NT << W) / N > 0 ? (NT << W) / N : 1;
     constexpr bool multipass = FftSchedule<L, W>::NP > 1;
-    return (TW_SMEM ? sizeof(float4) * N : 0) +
+    return (TW_SMEM ? sizeof(float2) * N : 0) +
            sizeof(float2) * (multipass ? static_cast<size_t>(RB) * sw_row_stride(N) : 0);
 }
 

@@ -50,8 +50,11 @@ constexpr int ilcm(int a, int b) {
 }
 
 template <int L_, int T_, int RLOG_, bool EXACT_, int FIR_REGS_ = 160, int FFT_REGS_ = 96,
-          int PC_ = 4, int FFT_WG_ = 2, int NTILE_ = 2>
+          int PC_ = 4, int FFT_WG_ = 2, int NTILE_ = 2, bool TW4_ = false>
 struct FusedCfg {
+    // twiddle table element: float2 (wr, wi), or pre-expanded float4 (fft.cuh tw_load)
+    static constexpr bool TW4 = TW4_;
+    using TwT = typename std::conditional<TW4_, float4, float2>::type;
     static constexpr int NTILE = NTILE_; // FFT tiles in flight between the roles
     static constexpr int L = L_, T = T_, RLOG = RLOG_;
     static constexpr bool EXACT = EXACT_;
@@ -75,7 +78,7 @@ struct FusedCfg {
     static constexpr unsigned STRIDE = sw_row_stride(N);
     static constexpr size_t CHUNK_BYTES = sizeof(float2) * size_t(B) * N;
     // shared-memory layout (bytes)
-    static constexpr size_t TW_BYTES = sizeof(float4) * N;
+    static constexpr size_t TW_BYTES = sizeof(TwT) * N;
     static constexpr size_t RING_OFF = (TW_BYTES + 127) & ~size_t(127);
     static constexpr size_t RING_BYTES = CHUNK_BYTES * G * PC;
     static constexpr size_t TILE_OFF = RING_OFF + RING_BYTES;
@@ -141,13 +144,13 @@ template <class Cfg, bool POWER = false>
 __global__ void __launch_bounds__(Cfg::NT, 1)
     fused_fir_fft_kernel(const float2* __restrict__ in, float2* __restrict__ out,
                          long long S_out, long long rows_per_cta, const float* __restrict__ taps,
-                         const float4* __restrict__ tw_g) {
+                         const typename Cfg::TwT* __restrict__ tw_g) {
     constexpr int L = Cfg::L, T = Cfg::T, RLOG = Cfg::RLOG, N = Cfg::N, R = Cfg::R;
     constexpr int NTG = Cfg::NTG, NFIR = Cfg::NFIR, NFFT = Cfg::NFFT, NT = Cfg::NT;
     constexpr int G = Cfg::G, B = Cfg::B;
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    float4* tw = reinterpret_cast<float4*>(smem_raw);
+    typename Cfg::TwT* tw = reinterpret_cast<typename Cfg::TwT*>(smem_raw);
     float2* ring = reinterpret_cast<float2*>(smem_raw + Cfg::RING_OFF);
     float2* tiles = reinterpret_cast<float2*>(smem_raw + Cfg::TILE_OFF);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + Cfg::BAR_OFF);
@@ -264,7 +267,7 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
     float4 twr[R > 1 ? R - 1 : 1];
 #pragma unroll
     for (int i = 0; i + 1 < R; ++i)
-        twr[i] = tw[i];
+        twr[i] = tw_load<true>(tw + i);
 
     const unsigned swj = sw(static_cast<unsigned>(j));
     for (long long b0 = 0; b0 < n_batches; b0 += BU) {

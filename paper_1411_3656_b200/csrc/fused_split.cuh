@@ -79,8 +79,11 @@ PPFG_DEV void set_max_regs() {
 }
 
 template <int L_, int LQ_, int T_, bool EXACT_, int FIR_WG_ = 2, int W_ = 5,
-          int FIR_REGS_ = 152, int FFT_REGS_ = 104, int PC_ = 0>
+          int FIR_REGS_ = 152, int FFT_REGS_ = 104, int PC_ = 0, bool TW4_ = false>
 struct SplitCfg {
+    // twiddle table element: float2 (wr, wi), or pre-expanded float4 (fft.cuh tw_load)
+    static constexpr bool TW4 = TW4_;
+    using TwT = typename std::conditional<TW4_, float4, float2>::type;
     static constexpr int L = L_, LQ = LQ_, T = T_;
     static constexpr bool EXACT = EXACT_;
     static constexpr int FIR_REGS = FIR_REGS_, FFT_REGS = FFT_REGS_;
@@ -103,8 +106,8 @@ struct SplitCfg {
     // tensor copy (3-D box {RUN, R, RB} of 8-byte elements)
     static constexpr size_t AVAIL = 232448 - 2 * TILE_BYTES - 512;
     // twiddles in shared memory when that still leaves >= 48 KB of ring
-    static constexpr bool TW_SMEM = sizeof(float4) * N + 48 * 1024 <= AVAIL;
-    static constexpr size_t TW_BYTES = TW_SMEM ? sizeof(float4) * N : 0;
+    static constexpr bool TW_SMEM = sizeof(TwT) * N + 48 * 1024 <= AVAIL;
+    static constexpr size_t TW_BYTES = TW_SMEM ? sizeof(TwT) * N : 0;
     static constexpr size_t RING_MAX = (AVAIL - TW_BYTES) < 96 * 1024 ? (AVAIL - TW_BYTES) : 96 * 1024;
     static constexpr size_t ROW_BYTES = sizeof(float2) * R * RUN; // one spectrum's runs
     // rows per chunk: the whole batch if two such chunks fit, else halves...
@@ -138,13 +141,14 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
     fused_split_kernel(const __grid_constant__ CUtensorMap in_map, const float2* __restrict__ in,
                        float2* __restrict__ out, long long S_out,
                        long long rows_per_cluster, const float* __restrict__ taps,
-                       const float4* __restrict__ tw_g) {
+                       const typename Cfg::TwT* __restrict__ tw_g) {
     constexpr int T = Cfg::T, N = Cfg::N, R = Cfg::R, RLOG = Cfg::RLOG, Q = Cfg::Q;
     constexpr int NFIR = Cfg::NFIR, NFFT = Cfg::NFFT, NT = Cfg::NT, B = Cfg::B, PC = Cfg::PC;
     constexpr int BU = Cfg::BU, RUN = Cfg::RUN;
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    float4* tw_s = reinterpret_cast<float4*>(smem_raw);
+    using TwT = typename Cfg::TwT;
+    TwT* tw_s = reinterpret_cast<TwT*>(smem_raw);
     float2* ring = reinterpret_cast<float2*>(smem_raw + Cfg::RING_OFF);
     float2* tiles = reinterpret_cast<float2*>(smem_raw + Cfg::TILE_OFF);
     uint64_t* ring_full = reinterpret_cast<uint64_t*>(smem_raw + Cfg::BAR_OFF);
@@ -186,7 +190,7 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
         // ================================ FFT role ================================
         set_max_regs<Cfg::FFT_REGS, Cfg::LAUNCH_REGS>();
         const int ftid = tid - NFIR;
-        const float4* tw = Cfg::TW_SMEM ? tw_s : tw_g;
+        const TwT* tw = Cfg::TW_SMEM ? tw_s : tw_g;
         const long long n_fills = n_batches / Q;
         for (long long f = 0; f < n_fills; ++f) {
             const int t = static_cast<int>(f & 1);
@@ -263,7 +267,7 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
     float4 twr[R > 1 ? R - 1 : 1];
 #pragma unroll
     for (int i = 0; i + 1 < R; ++i)
-        twr[i] = __ldg(tw_g + i);
+        twr[i] = tw_load<false>(tw_g + i);
 
     // tile slot offsets (float2 units) of this thread's channels
     unsigned slot_of[R];

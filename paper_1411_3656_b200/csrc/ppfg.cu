@@ -103,6 +103,7 @@ struct FusedEntry {
     int map_run = 0;
     KernelFn power_fn = nullptr; // detection variant (POWER), single-SM entries
     int power_rows = 0;          // its partials per CTA (tile rows)
+    bool tw4 = false;            // takes the pre-expanded float4 twiddle table
 };
 
 // The detection variant exists where the last FFT pass gives every FFT thread
@@ -117,6 +118,7 @@ template <class Cfg>
 FusedEntry fused_entry() {
     FusedEntry e{Cfg::L,    Cfg::T,  Cfg::EXACT, reinterpret_cast<KernelFn>(&fused_fir_fft_kernel<Cfg>),
                  Cfg::SMEM, Cfg::NT, Cfg::B * Cfg::G, 1, true};
+    e.tw4 = Cfg::TW4;
     if constexpr (has_power<Cfg>()) {
         e.power_fn = reinterpret_cast<KernelFn>(&fused_fir_fft_kernel<Cfg, true>);
         e.power_rows = static_cast<int>(Cfg::TILE_ROWS);
@@ -126,9 +128,11 @@ FusedEntry fused_entry() {
 
 template <class Cfg>
 FusedEntry split_entry(bool preferred) {
-    return {Cfg::L,    Cfg::T,  Cfg::EXACT, reinterpret_cast<KernelFn>(&fused_split_kernel<Cfg>),
-            Cfg::SMEM, Cfg::NT, Cfg::B,     Cfg::Q,
-            preferred, Cfg::R,  Cfg::RB,    Cfg::RUN};
+    FusedEntry e{Cfg::L,    Cfg::T,  Cfg::EXACT, reinterpret_cast<KernelFn>(&fused_split_kernel<Cfg>),
+                 Cfg::SMEM, Cfg::NT, Cfg::B,     Cfg::Q,
+                 preferred, Cfg::R,  Cfg::RB,    Cfg::RUN};
+    e.tw4 = Cfg::TW4;
+    return e;
 }
 
 // Which (C, T) get a fused kernel. Register budget per SM ~ C * (3T fp32 |
@@ -138,14 +142,16 @@ FusedEntry split_entry(bool preferred) {
 // elsewhere (round-1 sweep, profiles/round1/sweep.md).
 const std::vector<FusedEntry>& fused_table() {
     static const std::vector<FusedEntry> t = {
-        fused_entry<FusedCfg<10, 8, 2, false, 120, 80, 2, 3>>(),
+        // (float4 twiddle tables where they measured faster than float2:
+        // C=1024 T=8 FAST 0.86 vs 0.85 at the SKA size, C=512 EXACT 0.68 vs 0.65)
+        fused_entry<FusedCfg<10, 8, 2, false, 120, 80, 2, 3, 2, true>>(),
         fused_entry<FusedCfg<9, 8, 2, false>>(),
         fused_entry<FusedCfg<8, 8, 2, false>>(),
         fused_entry<FusedCfg<7, 8, 2, false>>(),
         fused_entry<FusedCfg<6, 8, 1, false, 120, 80, 2, 3>>(),
         fused_entry<FusedCfg<10, 4, 2, false>>(),
         fused_entry<FusedCfg<9, 16, 1, false>>(),
-        fused_entry<FusedCfg<9, 8, 1, true>>(),
+        fused_entry<FusedCfg<9, 8, 1, true, 160, 96, 4, 2, 2, true>>(),
         fused_entry<FusedCfg<8, 8, 1, true>>(),
         fused_entry<FusedCfg<7, 8, 1, true>>(),
         fused_entry<FusedCfg<6, 8, 1, true>>(),
@@ -169,12 +175,16 @@ const std::vector<FusedEntry>& fused_table() {
         // T=32 0.41 vs 0.18, FP64 T=8 0.62 vs 0.42, FP64 T=16 0.40 vs 0.32,
         // C=2048 0.51 vs 0.42, FP64 C=2048 0.47 vs 0.42, C=4096 0.43 vs 0.38;
         // C=8192 0.29 vs 0.32 stays opt-in via PPFG_CLUSTER)
-        split_entry<SplitCfg<10, 1, 16, false>>(true),
-        split_entry<SplitCfg<10, 2, 32, false>>(true),
+        // (float4 twiddle tables where they measured faster: FAST C=1024
+        // T=16 0.62 vs 0.58, EXACT C=1024 T=16 0.40 vs 0.39, EXACT C=2048
+        // 0.47 vs 0.44; FAST C=2048/4096 gained 15-27 % from float2)
+        // (T=32 FAST: the unfused K1b FP32 FIR -> FFT measured 0.43 vs 0.42)
+        split_entry<SplitCfg<10, 1, 16, false, 2, 5, 152, 104, 0, true>>(true),
+        split_entry<SplitCfg<10, 2, 32, false, 2, 5, 152, 104, 0, true>>(false),
         split_entry<SplitCfg<10, 1, 8, true>>(true),
-        split_entry<SplitCfg<10, 2, 16, true>>(true),
+        split_entry<SplitCfg<10, 2, 16, true, 2, 5, 152, 104, 0, true>>(true),
         split_entry<SplitCfg<11, 1, 8, false>>(true),
-        split_entry<SplitCfg<11, 2, 8, true>>(true),
+        split_entry<SplitCfg<11, 2, 8, true, 2, 5, 152, 104, 0, true>>(true),
         split_entry<SplitCfg<12, 2, 8, false>>(true),
         split_entry<SplitCfg<13, 3, 8, false>>(false),
 
@@ -351,7 +361,8 @@ struct ppfg_plan_s {
     int L = -1; // log2 C when C is a power of two
     int num_sms = 148;
     float* d_taps = nullptr;     // [T][C] f32
-    float4* d_tw = nullptr;      // FftPlan twiddles (wr, wi, -wi, wr), C-1 entries
+    float2* d_tw = nullptr;      // FftPlan twiddles (wr, wi), C-1 entries
+    float4* d_tw4 = nullptr;     // the same, pre-expanded (wr, wi, -wi, wr)
     double2* d_roots = nullptr;  // dft_naive roots, C entries (non-pow2)
     float* d_ones = nullptr;     // C unit taps: channelize through the T = 1 fused kernel
     const FusedEntry* fft_fused = nullptr;
@@ -378,15 +389,15 @@ namespace {
 
 // FftPlan twiddles exactly as dft.hpp:88-98: double angle -> cos/sin -> f32,
 // stored as (wr, wi, -wi, wr) for the packed butterfly (common.cuh bfly2).
-std::vector<float4> host_twiddles(uint64_t n) {
-    std::vector<float4> tw(n > 1 ? n - 1 : 1);
+std::vector<float2> host_twiddles(uint64_t n) {
+    std::vector<float2> tw(n > 1 ? n - 1 : 1);
     for (uint64_t len = 2; len <= n; len <<= 1) {
         const uint64_t half = len / 2;
         for (uint64_t j = 0; j < half; ++j) {
             const double angle = -2.0 * M_PI * static_cast<double>(j) / static_cast<double>(len);
             const float wr = static_cast<float>(std::cos(angle));
             const float wi = static_cast<float>(std::sin(angle));
-            tw[half - 1 + j] = make_float4(wr, wi, -wi, wr);
+            tw[half - 1 + j] = make_float2(wr, wi);
         }
     }
     return tw;
@@ -529,7 +540,7 @@ __global__ void fft_bitrev_kernel(const float2* in, float2* out, int L, long lon
     out[g] = in[row * N + (__brev(p) >> (32 - L))];
 }
 
-__global__ void fft_stage_kernel(float2* data, const float4* __restrict__ tw, int L, int s,
+__global__ void fft_stage_kernel(float2* data, const float2* __restrict__ tw, int L, int s,
                                  long long n_rows) {
     const long long g = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     const long long half = 1LL << (s - 1);
@@ -542,7 +553,7 @@ __global__ void fft_stage_kernel(float2* data, const float4* __restrict__ tw, in
     const long long base = (q >> (s - 1)) << s;
     float2* r = data + (row << L);
     float2 lo = r[base + j], hi = r[base + j + half];
-    bfly2(lo, hi, tw[half - 1 + j]);
+    bfly2(lo, hi, tw_expand(tw[half - 1 + j]));
     r[base + j] = lo;
     r[base + j + half] = hi;
 }
@@ -630,18 +641,21 @@ int launch_fused_entry(ppfg_plan p, const FusedEntry* e, const float* taps, uint
         if (e->map_r > 0) {
             CUtensorMap map;
             PPFG_TRY(encode_input_map(&map, din, p->C, S_in, e->map_r, e->map_rb, e->map_run));
-            void* args[] = {&map, &din, &dout, &S_out_ll, &rows_per_cluster, &taps, &p->d_tw};
+            void* tw = e->tw4 ? static_cast<void*>(p->d_tw4) : static_cast<void*>(p->d_tw);
+            void* args[] = {&map, &din, &dout, &S_out_ll, &rows_per_cluster, &taps, &tw};
             PPFG_CUDA(cudaLaunchKernelExC(&cfg, e->fn, args));
             return check_launch("fused split fir+fft kernel");
         }
-        void* args[] = {&din, &dout, &S_out_ll, &rows_per_cluster, &taps, &p->d_tw};
+        void* tw = e->tw4 ? static_cast<void*>(p->d_tw4) : static_cast<void*>(p->d_tw);
+        void* args[] = {&din, &dout, &S_out_ll, &rows_per_cluster, &taps, &tw};
         PPFG_CUDA(cudaLaunchKernelExC(&cfg, e->fn, args));
         return check_launch("fused cluster fir+fft kernel");
     }
     const uint64_t grid =
         std::max<uint64_t>(1, std::min<uint64_t>(p->num_sms, cdiv(S_out, e->rows_per_batch)));
     long long rows_per_cta = static_cast<long long>(cdiv(S_out, grid));
-    void* args[] = {&din, &dout, &S_out_ll, &rows_per_cta, &taps, &p->d_tw};
+    void* tw = e->tw4 ? static_cast<void*>(p->d_tw4) : static_cast<void*>(p->d_tw);
+    void* args[] = {&din, &dout, &S_out_ll, &rows_per_cta, &taps, &tw};
     PPFG_CUDA(cudaLaunchKernel(e->fn, dim3(static_cast<unsigned>(grid)), dim3(e->nt), args,
                                e->smem, st));
     return check_launch("fused fir+fft kernel");
@@ -831,7 +845,8 @@ int launch_fir_fft_mean_power(ppfg_plan p, const float2* din, uint64_t S_in, dou
         const int parts = static_cast<int>(grid) * e->power_rows;
         PPFG_TRY(ensure_parts(p, static_cast<size_t>(parts) * p->C * sizeof(double)));
         float2* part = reinterpret_cast<float2*>(p->d_part);
-        void* args[] = {&din, &part, &S_out_ll, &rows_per_cta, &p->d_taps, &p->d_tw};
+        void* tw = e->tw4 ? static_cast<void*>(p->d_tw4) : static_cast<void*>(p->d_tw);
+        void* args[] = {&din, &part, &S_out_ll, &rows_per_cta, &p->d_taps, &tw};
         PPFG_CUDA(cudaLaunchKernel(e->power_fn, dim3(static_cast<unsigned>(grid)), dim3(e->nt), args,
                                    e->smem, st));
         PPFG_TRY(check_launch("fused fir+fft+power kernel"));
@@ -1142,8 +1157,15 @@ int ppfg_plan_create(ppfg_plan* plan, uint64_t n_channels, uint64_t n_taps,
     }
     if (p->L >= 1) {
         const auto tw = host_twiddles(n_channels);
-        if (cudaMalloc(&p->d_tw, tw.size() * sizeof(float4)) != cudaSuccess ||
-            cudaMemcpy(p->d_tw, tw.data(), tw.size() * sizeof(float4), cudaMemcpyHostToDevice) !=
+        if (cudaMalloc(&p->d_tw, tw.size() * sizeof(float2)) != cudaSuccess ||
+            cudaMemcpy(p->d_tw, tw.data(), tw.size() * sizeof(float2), cudaMemcpyHostToDevice) !=
+                cudaSuccess)
+            return cleanup(fail(PPFG_CUDA_ERROR, "ppfg_plan_create: twiddle upload failed"));
+        std::vector<float4> tw4(tw.size());
+        for (size_t i = 0; i < tw.size(); ++i)
+            tw4[i] = make_float4(tw[i].x, tw[i].y, -tw[i].y, tw[i].x);
+        if (cudaMalloc(&p->d_tw4, tw4.size() * sizeof(float4)) != cudaSuccess ||
+            cudaMemcpy(p->d_tw4, tw4.data(), tw4.size() * sizeof(float4), cudaMemcpyHostToDevice) !=
                 cudaSuccess)
             return cleanup(fail(PPFG_CUDA_ERROR, "ppfg_plan_create: twiddle upload failed"));
     } else if (p->L < 0) {
@@ -1202,6 +1224,7 @@ int ppfg_plan_destroy(ppfg_plan p) {
         cudaStreamSynchronize(p->stream);
     cudaFree(p->d_taps);
     cudaFree(p->d_tw);
+    cudaFree(p->d_tw4);
     cudaFree(p->d_roots);
     cudaFree(p->d_ones);
     cudaFree(p->d_part);
