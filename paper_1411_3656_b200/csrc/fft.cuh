@@ -241,6 +241,90 @@ __global__ void __launch_bounds__(NT) fft_rows_kernel(const float2* in, float2* 
     }
 }
 
+// K2r: channelize_block for large power-of-two C (one row = 2^L c64 does not
+// leave room for K3's FIR/FFT tiles), one CTA per SM, rows strided over the
+// grid. Two row slots in shared memory, each loaded by ONE TMA bulk copy
+// (cp.async.bulk, SASS UBLKCP) of the natural-order row: while one slot's
+// row is transformed, the next row lands in the other, so HBM reads overlap
+// all three passes (K2 instead waits on its first pass's global loads).
+// Pass 1 reads the natural-order row (lanes = consecutive channels,
+// conflict-free) into registers — the whole row, one unit per thread — and,
+// after a barrier, writes it back IN PLACE at swizzled slots (the slot is
+// sized for the swizzled row); later passes are in place (each unit rewrites
+// its own elements) and the last stores bins to HBM. Twiddles (float2,
+// N - 1 entries) stay in shared memory. Same butterflies as K2: bit-exact.
+template <int L, int W>
+struct FftRing {
+    using S = FftSchedule<L, W>;
+    static constexpr int N = 1 << L;
+    static constexpr int W0 = S::width(0), LO0 = S::lo(0);
+    static constexpr int NT = N >> W0; // one first-pass unit per thread
+    static constexpr unsigned STRIDE = sw_row_stride(N);
+    static constexpr size_t TW_BYTES = sizeof(float2) * N;
+    static constexpr size_t SLOT_BYTES = (sizeof(float2) * STRIDE + 127) & ~size_t(127);
+    static constexpr size_t SMEM = TW_BYTES + 2 * SLOT_BYTES + 2 * sizeof(uint64_t);
+    static_assert(S::NP >= 2, "pass 1 hands over to FftPasses<.., I = 1>");
+};
+
+template <int L, int W>
+__global__ void __launch_bounds__(FftRing<L, W>::NT, 1)
+    fft_ring_kernel(const float2* __restrict__ in, float2* __restrict__ out, long long n_rows,
+                    const float2* __restrict__ tw_g) {
+    using F = FftRing<L, W>;
+    constexpr int N = F::N, NT = F::NT, W0 = F::W0, LO0 = F::LO0, E0 = 1 << W0;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    float2* tw = reinterpret_cast<float2*>(smem_raw);
+    float2* slots = reinterpret_cast<float2*>(smem_raw + F::TW_BYTES);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + F::TW_BYTES + 2 * F::SLOT_BYTES);
+    const int tid = threadIdx.x;
+    for (int i = tid; i < N - 1; i += NT)
+        tw[i] = tw_g[i];
+    if (tid == 0) {
+        mbar_init(full, 1);
+        mbar_init(full + 1, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const long long step = gridDim.x;
+    constexpr uint32_t ROW_BYTES = static_cast<uint32_t>(sizeof(float2) * N);
+    auto issue = [&](long long row, int s) {
+        mbar_arrive_expect_tx(full + s, ROW_BYTES);
+        bulk_g2s(reinterpret_cast<unsigned char*>(slots) + s * F::SLOT_BYTES, in + row * N, ROW_BYTES,
+                 full + s);
+    };
+    if (tid == 0) {
+        if (blockIdx.x < n_rows)
+            issue(blockIdx.x, 0);
+        if (blockIdx.x + step < n_rows)
+            issue(blockIdx.x + step, 1);
+    }
+    int i = 0;
+    for (long long row = blockIdx.x; row < n_rows; row += step, ++i) {
+        const int s = i & 1;
+        float2* slot = reinterpret_cast<float2*>(reinterpret_cast<unsigned char*>(slots) + s * F::SLOT_BYTES);
+        mbar_wait(full + s, static_cast<uint32_t>((i >> 1) & 1));
+        const unsigned fixed = static_cast<unsigned>(tid);
+        float2 v[E0];
+#pragma unroll
+        for (int k = 0; k < E0; ++k)
+            v[k] = slot[fixed + (static_cast<unsigned>(k) << LO0)];
+        fft_stages<L, LO0, W0, true>(v, fixed, tw);
+        __syncthreads(); // every natural-order read of the slot is done
+        float2* dst = slot + sw(fixed);
+#pragma unroll
+        for (int k = 0; k < E0; ++k)
+            dst[sw(static_cast<unsigned>(k) << LO0)] = v[k];
+        __syncthreads();
+        FftPasses<L, L, W, false, true, NT, 1>::run(nullptr, out, slot, F::STRIDE, 1,
+                                                    LinearRows{row, n_rows}, tw, tid, SyncCta{});
+        __syncthreads(); // every read of the slot is done: refill it
+        if (tid == 0 && row + 2 * step < n_rows) {
+            fence_proxy_async();
+            issue(row + 2 * step, s);
+        }
+    }
+}
+
 template <int L, int W, bool TW_SMEM, int NT>
 constexpr size_t fft_rows_smem_bytes() {
     constexpr int N = 1 << L;

@@ -693,6 +693,21 @@ int launch_channelize(ppfg_plan p, const float2* din, uint64_t rows, float2* dou
         return rc;
     }
     const int L = p->L;
+    // C = 8192: the TMA-ring row FFT (0.73 of the HBM roofline vs 0.57 for
+    // K2; at C = 4096 it measured 0.82 vs 0.83 for the T = 1 fused kernel)
+    if (L == 13 && reinterpret_cast<uintptr_t>(din) % 16 == 0) {
+        using F = FftRing<13, kFftW>;
+        KernelFn fn = reinterpret_cast<KernelFn>(&fft_ring_kernel<13, kFftW>);
+        PPFG_TRY(ensure_smem_attr(fn, F::SMEM, p->device));
+        int per_sm = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, F::NT, F::SMEM);
+        const uint64_t grid =
+            std::min<uint64_t>(rows, static_cast<uint64_t>(p->num_sms) * std::max(per_sm, 1));
+        long long rows_ll = static_cast<long long>(rows);
+        void* args[] = {&din, &dout, &rows_ll, &p->d_tw};
+        PPFG_CUDA(cudaLaunchKernel(fn, dim3(static_cast<unsigned>(grid)), dim3(F::NT), args, F::SMEM, st));
+        return check_launch("fft kernel (TMA ring)");
+    }
     // T = 1 fused kernel with unit taps (in place is safe: row s is written
     // only after it was read, and nothing else reads it); TMA needs a
     // 16-byte-aligned source
