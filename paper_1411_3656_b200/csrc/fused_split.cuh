@@ -133,7 +133,7 @@ struct SplitCfg {
     static_assert(PC >= 2, "input ring too shallow");
     static_assert(B % RB == 0, "whole chunks per batch");
     static_assert(RUN <= 256 && R <= 256 && RB <= 256, "TMA box dimensions");
-    static_assert(BU * B <= 32, "FIR unroll too large");
+    static_assert(BU * B <= 64, "FIR unroll too large");
 };
 
 template <class Cfg>
