@@ -147,6 +147,24 @@ def test_fft_bitwise_vs_oracle(cuda, port, L):
     assert np.array_equal(bits(got), bits(port.channelize(x, n)))
 
 
+# K2r (C = 8192): many rows per CTA, so both row slots are reused with
+# alternating mbarrier phases; in place and out of place.
+@pytest.mark.parametrize("rows", [1, 2, 149, 700])
+def test_fft_ring_many_rows(cuda, port, rows):
+    import torch
+    ppf = ppf_mod()
+    n = 8192
+    rng = np.random.default_rng(rows)
+    x = uniform(rng, rows * n)
+    want = bits(port.channelize(x, n))
+    assert np.array_equal(bits(ppf.channelize_block(x, n)), want)
+    xd = torch.from_numpy(x.view(np.complex64).reshape(rows, n)).cuda()
+    with ppf.Plan(n, 0) as p:
+        p.channelize(xd, out=xd)   # in place
+    torch.cuda.synchronize()
+    assert np.array_equal(bits(xd.cpu().numpy()), want)
+
+
 def test_fft_api_semantics(cuda, port):
     """dft_test.cpp:72-123, 125-197."""
     ppf = ppf_mod()
@@ -193,7 +211,8 @@ def test_fused_golden_exact(cuda, golden):
 
 
 @pytest.mark.parametrize("C,T", [(512, 8), (1024, 8), (64, 8), (256, 4), (2048, 8), (8192, 8), (4096, 8), (1024, 32),
-                                 (1024, 4), (1024, 16), (512, 16), (128, 8), (1024, 64), (256, 128)])
+                                 (1024, 4), (1024, 16), (512, 16), (128, 8), (1024, 64), (256, 128),
+                                 (256, 8)])
 @pytest.mark.parametrize("flags", ["exact", "fast", "exact+cluster", "fast+cluster", "fast+unfused"])
 def test_fused_vs_oracle(cuda, port, C, T, flags):
     ppf = ppf_mod()
@@ -398,7 +417,8 @@ def test_mean_power_empty(cuda):
 
 @pytest.mark.parametrize("C,T,flags", [(1024, 8, "fast"), (512, 8, "exact"), (1024, 4, "fast"),
                                        (512, 16, "fast"), (1024, 16, "fast"), (100, 4, "exact"),
-                                       (2048, 8, "exact")])
+                                       (2048, 8, "exact"), (128, 8, "fast"), (256, 8, "exact"),
+                                       (256, 8, "fast")])
 def test_fir_fft_mean_power(cuda, port, C, T, flags):
     """Fused detection (bins never written where a detection kernel exists)
     == mean_power(fir_fft(x)) == the oracle's inspect of the oracle's bins."""
