@@ -18,7 +18,11 @@ for spec in sys.argv[1:]:
     x = torch.empty((S, C), dtype=torch.complex64, device="cuda"); ppf.synth(C, S * C, seed=3, out=x)
     y = torch.empty((S - T + 1, C), dtype=torch.complex64, device="cuda")
     c = ppf.generate_prototype(C, T)
-    if mode == "fft":
+    if mode == "fir":   # FIR only (bit-exact)
+        with ppf.Plan(C, T, c) as p:
+            t = timeit(lambda: p.fir(x, out=y))
+        B = (2 * S - T + 1) * C * 8
+    elif mode == "fft":
         with ppf.Plan(C, 1, ppf.generate_prototype(C, 1)) as p:
             t = timeit(lambda: p.channelize(x, out=x))
         B = 2 * S * C * 8
