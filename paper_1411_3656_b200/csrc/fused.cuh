@@ -84,6 +84,17 @@ struct FusedCfg {
     static constexpr size_t TILE_OFF = RING_OFF + RING_BYTES;
     static constexpr size_t TILE_ROWS = size_t(G) * B;
     static constexpr size_t TILE_BYTES = sizeof(float2) * TILE_ROWS * STRIDE;
+    // FFT pass groups: one per warpgroup where the tile's rows split evenly
+    static constexpr bool FFT_SPLIT = TILE_ROWS % FFT_WG_ == 0;
+    static constexpr int PNT = FFT_SPLIT ? 128 : NFFT;  // threads per pass group
+    static constexpr int PROWS = FFT_SPLIT ? int(TILE_ROWS) / FFT_WG_ : int(TILE_ROWS);
+    static constexpr int PGROUPS = FFT_SPLIT ? FFT_WG_ : 1;
+    // detection (POWER): last-pass units per row; a thread's units all have
+    // the same bins when PNT is a multiple of it, so its FP64 accumulators
+    // stay per bin — partial rows per CTA: PNT / UL per pass group
+    static constexpr int UL = N >> FftSchedule<L - RLOG, W>::width(FftSchedule<L - RLOG, W>::NP - 1);
+    static constexpr bool POWER_OK = T > 1 && PNT % UL == 0;
+    static constexpr int POWER_ROWS = PGROUPS * (PNT / UL);
     static constexpr size_t BAR_OFF = (TILE_OFF + NTILE * TILE_BYTES + 7) & ~size_t(7);
     static constexpr size_t SMEM = BAR_OFF + sizeof(uint64_t) * 2 * G * PC;
     static_assert(NTG >= 32 && NTG <= NFIR && NFIR % NTG == 0, "FIR groups must be whole warps");
@@ -179,9 +190,8 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(Cfg::FFT_REGS));
         const int ftid = tid - NFIR;
         // per-warpgroup rows where the tile splits evenly, else CTA-wide passes
-        constexpr bool SPLIT = Cfg::TILE_ROWS % Cfg::FFT_WG == 0;
-        constexpr int PNT = SPLIT ? 128 : NFFT;                 // threads per pass group
-        constexpr int PROWS = SPLIT ? Cfg::TILE_ROWS / Cfg::FFT_WG : Cfg::TILE_ROWS;
+        constexpr bool SPLIT = Cfg::FFT_SPLIT;
+        constexpr int PNT = Cfg::PNT, PROWS = Cfg::PROWS;
         const int pg = SPLIT ? ftid / 128 : 0;                  // pass group
         const int ptid = ftid - pg * PNT;
         using Passes = FftPasses<L, L - RLOG, Cfg::W, false, true, PNT, 0, true, POWER>;
@@ -200,14 +210,14 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
             named_arrive(1 + Cfg::NTILE + t, NT);
         }
         if constexpr (POWER) {
-            // the last pass gives each thread exactly one unit: tile row r,
-            // bins u + rev_L(k)
+            // every last-pass unit of this thread (tile rows ptid / UL +
+            // m * PNT / UL) covers bins u + rev_L(k): partial row r of the CTA
             constexpr int UL = N / EL;
-            static_assert(PROWS * UL == PNT, "one last-pass unit per FFT thread");
-            const int r = pg * PROWS + ptid / UL;
+            static_assert(UL == Cfg::UL && Cfg::POWER_OK, "per-bin accumulators");
+            const int r = pg * (PNT / UL) + ptid / UL;
             const unsigned u = static_cast<unsigned>(ptid % UL);
             double* part = reinterpret_cast<double*>(out) +
-                           (static_cast<size_t>(blockIdx.x) * Cfg::TILE_ROWS + r) * N + u;
+                           (static_cast<size_t>(blockIdx.x) * Cfg::POWER_ROWS + r) * N + u;
 #pragma unroll
             for (int k = 0; k < EL; ++k)
                 part[crev(static_cast<unsigned>(k), L)] = pacc[k];

@@ -106,12 +106,11 @@ struct FusedEntry {
     bool tw4 = false;            // takes the pre-expanded float4 twiddle table
 };
 
-// The detection variant exists where the last FFT pass gives every FFT thread
-// exactly one unit (its accumulators then always see the same bins).
+// The detection variant exists where every FFT thread's last-pass units see
+// the same bins (FusedCfg::POWER_OK), so its accumulators stay per bin.
 template <class Cfg>
 constexpr bool has_power() {
-    using P = FftPasses<Cfg::L, Cfg::L - Cfg::RLOG, Cfg::W, false, true, Cfg::NFFT, 0, true, true>;
-    return Cfg::T > 1 && Cfg::TILE_ROWS * (Cfg::N / P::E_LAST) == Cfg::NFFT;
+    return Cfg::POWER_OK;
 }
 
 template <class Cfg>
@@ -121,7 +120,7 @@ FusedEntry fused_entry() {
     e.tw4 = Cfg::TW4;
     if constexpr (has_power<Cfg>()) {
         e.power_fn = reinterpret_cast<KernelFn>(&fused_fir_fft_kernel<Cfg, true>);
-        e.power_rows = static_cast<int>(Cfg::TILE_ROWS);
+        e.power_rows = Cfg::POWER_ROWS;
     }
     return e;
 }

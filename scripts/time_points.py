@@ -18,7 +18,11 @@ for spec in sys.argv[1:]:
     x = torch.empty((S, C), dtype=torch.complex64, device="cuda"); ppf.synth(C, S * C, seed=3, out=x)
     y = torch.empty((S - T + 1, C), dtype=torch.complex64, device="cuda")
     c = ppf.generate_prototype(C, T)
-    if mode == "fir":   # FIR only (bit-exact)
+    if mode in ("detect", "detect-exact"):   # fused FIR+FFT+mean power: input bytes only
+        with ppf.Plan(C, T, c, flags=ppf.FAST if mode == "detect" else ppf.EXACT) as p:
+            t = timeit(lambda: p.fir_fft_mean_power(x))
+        B = S * C * 8
+    elif mode == "fir":   # FIR only (bit-exact)
         with ppf.Plan(C, T, c) as p:
             t = timeit(lambda: p.fir(x, out=y))
         B = (2 * S - T + 1) * C * 8
