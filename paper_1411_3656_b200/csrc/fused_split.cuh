@@ -125,6 +125,11 @@ struct SplitCfg {
     // ring_full[PC], ring_empty[PC], full[2], empty[Q][2]
     static constexpr size_t SMEM = BAR_OFF + BARS;
     static constexpr uint32_t REMOTE_BYTES = uint32_t(sizeof(float2)) * (Q - 1) * B * (N / Q);
+    // detection (POWER): as fused.cuh — last-pass units per row, per-bin
+    // accumulators when the FFT role's thread count is a multiple of it
+    static constexpr int UL = N >> FftSchedule<LREM, W>::width(FftSchedule<LREM, W>::NP - 1);
+    static constexpr bool POWER_OK = NFFT % UL == 0;
+    static constexpr int POWER_ROWS = NFFT / UL;
     static_assert(Q >= 2 && Q <= 8, "portable cluster sizes");
     static_assert(R >= 1 && R <= 8 && R * Q * NFIR == N, "every FIR thread owns whole channels");
     static constexpr int LAUNCH_REGS = (65536 / NT) & ~7;
@@ -136,7 +141,9 @@ struct SplitCfg {
     static_assert(BU * B <= 64, "FIR unroll too large");
 };
 
-template <class Cfg>
+// POWER: the detection variant — `out` receives per-CTA partial power sums
+// (POWER_ROWS rows of N doubles per CTA) instead of the bins.
+template <class Cfg, bool POWER = false>
 __global__ void __launch_bounds__(Cfg::NT, 1)
     fused_split_kernel(const __grid_constant__ CUtensorMap in_map, const float2* __restrict__ in,
                        float2* __restrict__ out, long long S_out,
@@ -192,6 +199,10 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
         const int ftid = tid - NFIR;
         const TwT* tw = Cfg::TW_SMEM ? tw_s : tw_g;
         const long long n_fills = n_batches / Q;
+        double pacc[POWER ? (N / Cfg::UL) : 1];
+#pragma unroll
+        for (int k = 0; k < (POWER ? N / Cfg::UL : 1); ++k)
+            pacc[k] = 0.0;
         for (long long f = 0; f < n_fills; ++f) {
             const int t = static_cast<int>(f & 1);
             const long long b = f * Q + rank;
@@ -201,9 +212,9 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
             if (ftid == 0) PPFG_TR(1, f, 1);
             mbar_wait(full + t, static_cast<uint32_t>((f >> 1) & 1)); // remote blocks landed
             if (ftid == 0) PPFG_TR(1, f, 2);
-            FftPasses<Cfg::L, Cfg::LREM, Cfg::W, false, Cfg::TW_SMEM, NFFT>::run(
+            FftPasses<Cfg::L, Cfg::LREM, Cfg::W, false, Cfg::TW_SMEM, NFFT, 0, true, POWER>::run(
                 nullptr, out, tile, Cfg::STRIDE, B, FusedRows{o0, o1, rows, b * B, B}, tw, ftid,
-                SyncNamed{5, NFFT});
+                SyncNamed{5, NFFT}, pacc);
             named_sync(5, NFFT); // every read of the tile has completed
             if (ftid == 0) PPFG_TR(1, f, 3);
             if (ftid == 0) {
@@ -213,6 +224,17 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
                 for (int q = 0; q < Q; ++q)
                     mbar_arrive_remote_relaxed(mapa(e, static_cast<uint32_t>(q)));
             }
+        }
+        if constexpr (POWER) {
+            static_assert(Cfg::POWER_OK, "per-bin accumulators");
+            constexpr int UL = Cfg::UL, EL = N / UL;
+            const int r = ftid / UL;
+            const unsigned u = static_cast<unsigned>(ftid % UL);
+            double* part = reinterpret_cast<double*>(out) +
+                           (static_cast<size_t>(blockIdx.x) * Cfg::POWER_ROWS + r) * N + u;
+#pragma unroll
+            for (int k = 0; k < EL; ++k)
+                part[crev(static_cast<unsigned>(k), Cfg::L)] = pacc[k];
         }
         cluster_sync_all();
         return;

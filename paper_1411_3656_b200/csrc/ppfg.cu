@@ -131,6 +131,10 @@ FusedEntry split_entry(bool preferred) {
                  Cfg::SMEM, Cfg::NT, Cfg::B,     Cfg::Q,
                  preferred, Cfg::R,  Cfg::RB,    Cfg::RUN};
     e.tw4 = Cfg::TW4;
+    if constexpr (Cfg::POWER_OK) {
+        e.power_fn = reinterpret_cast<KernelFn>(&fused_split_kernel<Cfg, true>);
+        e.power_rows = Cfg::POWER_ROWS;
+    }
     return e;
 }
 
@@ -613,9 +617,14 @@ int encode_rows_map(CUtensorMap* map, const float2* din, uint64_t C, uint64_t S_
     return PPFG_OK;
 }
 
+// fn: the kernel to launch (default e->fn; e->power_fn for detection, whose
+// dout is the partials buffer); *grid_out receives the CTA count
 int launch_fused_entry(ppfg_plan p, const FusedEntry* e, const float* taps, uint64_t T,
-                       const float2* din, uint64_t S_in, float2* dout, cudaStream_t st) {
-    PPFG_TRY(ensure_smem_attr(e->fn, e->smem, p->device));
+                       const float2* din, uint64_t S_in, float2* dout, cudaStream_t st,
+                       KernelFn fn = nullptr, uint64_t* grid_out = nullptr) {
+    if (!fn)
+        fn = e->fn;
+    PPFG_TRY(ensure_smem_attr(fn, e->smem, p->device));
     const uint64_t S_out = S_in - T + 1;
     long long S_out_ll = static_cast<long long>(S_out);
     if (e->q > 1) {
@@ -633,32 +642,36 @@ int launch_fused_entry(ppfg_plan p, const FusedEntry* e, const float* taps, uint
         cfg.numAttrs = 1;
         cfg.gridDim = dim3(p->num_sms / e->q * e->q);
         int max_clusters = 0;
-        PPFG_CUDA(cudaOccupancyMaxActiveClusters(&max_clusters, e->fn, &cfg));
+        PPFG_CUDA(cudaOccupancyMaxActiveClusters(&max_clusters, fn, &cfg));
         if (max_clusters < 1)
             return fail(PPFG_CUDA_ERROR, "fused cluster kernel: no cluster fits an SM group");
         const uint64_t n_clusters = std::max<uint64_t>(
             1, std::min<uint64_t>(max_clusters, cdiv(S_out, e->rows_per_batch)));
         cfg.gridDim = dim3(static_cast<unsigned>(n_clusters * e->q));
+        if (grid_out)
+            *grid_out = n_clusters * e->q;
         long long rows_per_cluster = static_cast<long long>(cdiv(S_out, n_clusters));
         if (e->map_r > 0) {
             CUtensorMap map;
             PPFG_TRY(encode_input_map(&map, din, p->C, S_in, e->map_r, e->map_rb, e->map_run));
             void* tw = e->tw4 ? static_cast<void*>(p->d_tw4) : static_cast<void*>(p->d_tw);
             void* args[] = {&map, &din, &dout, &S_out_ll, &rows_per_cluster, &taps, &tw};
-            PPFG_CUDA(cudaLaunchKernelExC(&cfg, e->fn, args));
+            PPFG_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
             return check_launch("fused split fir+fft kernel");
         }
         void* tw = e->tw4 ? static_cast<void*>(p->d_tw4) : static_cast<void*>(p->d_tw);
         void* args[] = {&din, &dout, &S_out_ll, &rows_per_cluster, &taps, &tw};
-        PPFG_CUDA(cudaLaunchKernelExC(&cfg, e->fn, args));
+        PPFG_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
         return check_launch("fused cluster fir+fft kernel");
     }
     const uint64_t grid =
         std::max<uint64_t>(1, std::min<uint64_t>(p->num_sms, cdiv(S_out, e->rows_per_batch)));
     long long rows_per_cta = static_cast<long long>(cdiv(S_out, grid));
+    if (grid_out)
+        *grid_out = grid;
     void* tw = e->tw4 ? static_cast<void*>(p->d_tw4) : static_cast<void*>(p->d_tw);
     void* args[] = {&din, &dout, &S_out_ll, &rows_per_cta, &taps, &tw};
-    PPFG_CUDA(cudaLaunchKernel(e->fn, dim3(static_cast<unsigned>(grid)), dim3(e->nt), args,
+    PPFG_CUDA(cudaLaunchKernel(fn, dim3(static_cast<unsigned>(grid)), dim3(e->nt), args,
                                e->smem, st));
     return check_launch("fused fir+fft kernel");
 }
@@ -854,20 +867,12 @@ int launch_fir_fft_mean_power(ppfg_plan p, const float2* din, uint64_t S_in, dou
     const uint64_t S_out = S_in - p->T + 1;
     const FusedEntry* e = p->fused;
     if (e && e->power_fn && !(p->flags & PPFG_UNFUSED) && aligned16(din)) {
-        PPFG_TRY(ensure_smem_attr(e->power_fn, e->smem, p->device));
-        const uint64_t grid =
-            std::max<uint64_t>(1, std::min<uint64_t>(p->num_sms, cdiv(S_out, e->rows_per_batch)));
-        long long rows_per_cta = static_cast<long long>(cdiv(S_out, grid));
-        long long S_out_ll = static_cast<long long>(S_out);
-        const int parts = static_cast<int>(grid) * e->power_rows;
-        PPFG_TRY(ensure_parts(p, static_cast<size_t>(parts) * p->C * sizeof(double)));
-        float2* part = reinterpret_cast<float2*>(p->d_part);
-        void* tw = e->tw4 ? static_cast<void*>(p->d_tw4) : static_cast<void*>(p->d_tw);
-        void* args[] = {&din, &part, &S_out_ll, &rows_per_cta, &p->d_taps, &tw};
-        PPFG_CUDA(cudaLaunchKernel(e->power_fn, dim3(static_cast<unsigned>(grid)), dim3(e->nt), args,
-                                   e->smem, st));
-        PPFG_TRY(check_launch("fused fir+fft+power kernel"));
-        return launch_power_reduce(p, parts, S_out, dmean, st);
+        // partials: at most one CTA per SM, power_rows rows of C doubles each
+        PPFG_TRY(ensure_parts(p, static_cast<size_t>(p->num_sms) * e->power_rows * p->C * sizeof(double)));
+        uint64_t grid = 0;
+        PPFG_TRY(launch_fused_entry(p, e, p->d_taps, p->T, din, S_in,
+                                    reinterpret_cast<float2*>(p->d_part), st, e->power_fn, &grid));
+        return launch_power_reduce(p, static_cast<int>(grid) * e->power_rows, S_out, dmean, st);
     }
     // bins through a plan-owned (grow-only) buffer; the stream orders reuse
     const size_t bytes = S_out * p->C * sizeof(float2);

@@ -419,7 +419,8 @@ def test_mean_power_empty(cuda):
                                        (512, 16, "fast"), (1024, 16, "fast"), (100, 4, "exact"),
                                        (2048, 8, "exact"), (128, 8, "fast"), (256, 8, "exact"),
                                        (256, 8, "fast"), (64, 8, "fast"), (64, 8, "exact"),
-                                       (128, 8, "exact"), (1024, 4, "exact")])
+                                       (128, 8, "exact"), (1024, 4, "exact"), (4096, 8, "fast"),
+                                       (1024, 8, "exact")])
 def test_fir_fft_mean_power(cuda, port, C, T, flags):
     """Fused detection (bins never written where a detection kernel exists)
     == mean_power(fir_fft(x)) == the oracle's inspect of the oracle's bins."""
