@@ -253,12 +253,14 @@ __global__ void __launch_bounds__(NT) fft_rows_kernel(const float2* in, float2* 
 // sized for the swizzled row); later passes are in place (each unit rewrites
 // its own elements) and the last stores bins to HBM. Twiddles (float2,
 // N - 1 entries) stay in shared memory. Same butterflies as K2: bit-exact.
-template <int L, int W>
+template <int L, int W, int NT_ = 0>
 struct FftRing {
     using S = FftSchedule<L, W>;
     static constexpr int N = 1 << L;
     static constexpr int W0 = S::width(0), LO0 = S::lo(0);
-    static constexpr int NT = N >> W0; // one first-pass unit per thread
+    static constexpr int U0 = N >> W0;                // first-pass units: the whole row
+    static constexpr int NT = NT_ > 0 ? NT_ : U0;     // (threads >= U0 idle in pass 1)
+    static_assert(NT >= U0, "pass 1 holds the whole row in registers");
     static constexpr unsigned STRIDE = sw_row_stride(N);
     static constexpr size_t TW_BYTES = sizeof(float2) * N;
     static constexpr size_t SLOT_BYTES = (sizeof(float2) * STRIDE + 127) & ~size_t(127);
@@ -266,11 +268,11 @@ struct FftRing {
     static_assert(S::NP >= 2, "pass 1 hands over to FftPasses<.., I = 1>");
 };
 
-template <int L, int W>
-__global__ void __launch_bounds__(FftRing<L, W>::NT, 1)
+template <int L, int W, int NT_ = 0>
+__global__ void __launch_bounds__(FftRing<L, W, NT_>::NT, 1)
     fft_ring_kernel(const float2* __restrict__ in, float2* __restrict__ out, long long n_rows,
                     const float2* __restrict__ tw_g) {
-    using F = FftRing<L, W>;
+    using F = FftRing<L, W, NT_>;
     constexpr int N = F::N, NT = F::NT, W0 = F::W0, LO0 = F::LO0, E0 = 1 << W0;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     float2* tw = reinterpret_cast<float2*>(smem_raw);
@@ -303,17 +305,22 @@ __global__ void __launch_bounds__(FftRing<L, W>::NT, 1)
         const int s = i & 1;
         float2* slot = reinterpret_cast<float2*>(reinterpret_cast<unsigned char*>(slots) + s * F::SLOT_BYTES);
         mbar_wait(full + s, static_cast<uint32_t>((i >> 1) & 1));
-        const unsigned fixed = static_cast<unsigned>(tid);
+        const bool p1 = tid < F::U0;
+        const unsigned fixed = static_cast<unsigned>(p1 ? tid : 0);
         float2 v[E0];
+        if (p1) {
 #pragma unroll
-        for (int k = 0; k < E0; ++k)
-            v[k] = slot[fixed + (static_cast<unsigned>(k) << LO0)];
-        fft_stages<L, LO0, W0, true>(v, fixed, tw);
+            for (int k = 0; k < E0; ++k)
+                v[k] = slot[fixed + (static_cast<unsigned>(k) << LO0)];
+            fft_stages<L, LO0, W0, true>(v, fixed, tw);
+        }
         __syncthreads(); // every natural-order read of the slot is done
-        float2* dst = slot + sw(fixed);
+        if (p1) {
+            float2* dst = slot + sw(fixed);
 #pragma unroll
-        for (int k = 0; k < E0; ++k)
-            dst[sw(static_cast<unsigned>(k) << LO0)] = v[k];
+            for (int k = 0; k < E0; ++k)
+                dst[sw(static_cast<unsigned>(k) << LO0)] = v[k];
+        }
         __syncthreads();
         FftPasses<L, L, W, false, true, NT, 1>::run(nullptr, out, slot, F::STRIDE, 1,
                                                     LinearRows{row, n_rows}, tw, tid, SyncCta{});

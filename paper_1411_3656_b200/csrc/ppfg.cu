@@ -208,6 +208,7 @@ struct FftEntry {
 constexpr int kFftW = 5;
 constexpr int kFftNT = 256;
 constexpr int kFftMaxL = 13;
+constexpr int kRingNT = 0; // K2r threads per CTA (0: one first-pass unit per thread; 512 measured the same)
 
 template <int L>
 FftEntry fft_entry() {
@@ -711,8 +712,8 @@ int launch_channelize(ppfg_plan p, const float2* din, uint64_t rows, float2* dou
     // C = 8192: the TMA-ring row FFT (0.73 of the HBM roofline vs 0.57 for
     // K2; at C = 4096 it measured 0.82 vs 0.83 for the T = 1 fused kernel)
     if (L == 13 && reinterpret_cast<uintptr_t>(din) % 16 == 0) {
-        using F = FftRing<13, kFftW>;
-        KernelFn fn = reinterpret_cast<KernelFn>(&fft_ring_kernel<13, kFftW>);
+        using F = FftRing<13, kFftW, kRingNT>;
+        KernelFn fn = reinterpret_cast<KernelFn>(&fft_ring_kernel<13, kFftW, kRingNT>);
         PPFG_TRY(ensure_smem_attr(fn, F::SMEM, p->device));
         int per_sm = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, F::NT, F::SMEM);
