@@ -241,7 +241,8 @@ __global__ void __launch_bounds__(NT) fft_rows_kernel(const float2* in, float2* 
     }
 }
 
-// K2r: channelize_block for large power-of-two C (one row = 2^L c64 does not
+// K2r: channelize_block (dft.hpp:175-235; FftPlan::transform, dft.hpp:100-148)
+// for large power-of-two C (one row = 2^L c64 does not
 // leave room for K3's FIR/FFT tiles), one CTA per SM, rows strided over the
 // grid. Two row slots in shared memory, each loaded by ONE TMA bulk copy
 // (cp.async.bulk, SASS UBLKCP) of the natural-order row: while one slot's

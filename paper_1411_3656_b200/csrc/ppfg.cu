@@ -162,6 +162,21 @@ const std::vector<FusedEntry>& fused_table() {
         fused_entry<FusedCfg<7, 8, 1, true, 160, 96, 4, 2, 2, true>>(),
         fused_entry<FusedCfg<6, 8, 1, true, 160, 96, 4, 2, 2, true>>(),
         fused_entry<FusedCfg<10, 4, 2, true>>(),
+        // small C at T = 4 and 16 (register budget: 3T·R FP32, 6T·R FP64 per FIR thread)
+        fused_entry<FusedCfg<8, 16, 1, false>>(),
+        fused_entry<FusedCfg<7, 16, 1, false>>(),
+        fused_entry<FusedCfg<6, 16, 1, false>>(),
+        fused_entry<FusedCfg<8, 16, 0, true>>(),
+        fused_entry<FusedCfg<7, 16, 0, true>>(),
+        fused_entry<FusedCfg<6, 16, 0, true>>(),
+        fused_entry<FusedCfg<9, 4, 2, false>>(),
+        fused_entry<FusedCfg<8, 4, 2, false>>(),
+        fused_entry<FusedCfg<7, 4, 2, false>>(),
+        fused_entry<FusedCfg<6, 4, 1, false>>(),
+        fused_entry<FusedCfg<9, 4, 2, true>>(),
+        fused_entry<FusedCfg<8, 4, 2, true>>(),
+        fused_entry<FusedCfg<7, 4, 2, true>>(),
+        fused_entry<FusedCfg<6, 4, 1, true>>(),
         // T = 1 with unit taps: x*1 == x exactly, so these are bit-exact,
         // TMA-fed, warp-specialised FFTs — channelize_block for 64 <= C <= 4096
         // (C = 4096: 0.76 of roofline vs 0.69 for K2)
