@@ -177,6 +177,9 @@ const std::vector<FusedEntry>& fused_table() {
         fused_entry<FusedCfg<8, 4, 2, true>>(),
         fused_entry<FusedCfg<7, 4, 2, true>>(),
         fused_entry<FusedCfg<6, 4, 1, true>>(),
+        fused_entry<FusedCfg<8, 32, 0, false>>(),
+        fused_entry<FusedCfg<7, 32, 0, false>>(),
+        fused_entry<FusedCfg<6, 32, 0, false>>(),
         // T = 1 with unit taps: x*1 == x exactly, so these are bit-exact,
         // TMA-fed, warp-specialised FFTs — channelize_block for 64 <= C <= 4096
         // (C = 4096: 0.76 of roofline vs 0.69 for K2)

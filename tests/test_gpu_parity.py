@@ -212,7 +212,8 @@ def test_fused_golden_exact(cuda, golden):
 
 @pytest.mark.parametrize("C,T", [(512, 8), (1024, 8), (64, 8), (256, 4), (2048, 8), (8192, 8), (4096, 8), (1024, 32),
                                  (1024, 4), (1024, 16), (512, 16), (128, 8), (1024, 64), (256, 128),
-                                 (256, 8), (64, 4), (128, 16), (256, 16), (64, 16), (512, 4), (128, 4)])
+                                 (256, 8), (64, 4), (128, 16), (256, 16), (64, 16), (512, 4), (128, 4), (256, 32),
+                                 (64, 32)])
 @pytest.mark.parametrize("flags", ["exact", "fast", "exact+cluster", "fast+cluster", "fast+unfused"])
 def test_fused_vs_oracle(cuda, port, C, T, flags):
     ppf = ppf_mod()
