@@ -169,6 +169,12 @@ PPFG_DEV void bulk_g2s(void* smem_dst, const void* gmem_src, uint32_t bytes, uin
         : "memory");
 }
 
+// L2 prefetch of a global range (cp.async.bulk.prefetch.L2; no shared memory,
+// no completion tracking): warms L2 for a later bulk copy of the same bytes
+PPFG_DEV void bulk_prefetch_l2(const void* gmem_src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gmem_src), "r"(bytes) : "memory");
+}
+
 // streaming (evict-first) 8-byte global store
 PPFG_DEV void st_cs(float2* p, float2 v) { __stcs(p, v); }
 

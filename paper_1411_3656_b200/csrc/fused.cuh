@@ -50,8 +50,12 @@ constexpr int ilcm(int a, int b) {
 }
 
 template <int L_, int T_, int RLOG_, bool EXACT_, int FIR_REGS_ = 160, int FFT_REGS_ = 96,
-          int PC_ = 4, int FFT_WG_ = 2, int NTILE_ = 2, bool TW4_ = false>
+          int PC_ = 4, int FFT_WG_ = 2, int NTILE_ = 2, bool TW4_ = false, int L2A_ = 0>
 struct FusedCfg {
+    // L2A > 0: the producer also prefetches (cp.async.bulk.prefetch.L2) the
+    // chunk L2A past the one it copies into the ring, so that chunk's bulk
+    // copy later starts from L2 — lookahead without shared memory
+    static constexpr int L2A = L2A_;
     // twiddle table element: float2 (wr, wi), or pre-expanded float4 (fft.cuh tw_load)
     static constexpr bool TW4 = TW4_;
     using TwT = typename std::conditional<TW4_, float4, float2>::type;
@@ -251,6 +255,15 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
         mbar_arrive_expect_tx(full_g + slot, bytes);
         bulk_g2s(ring_g + static_cast<size_t>(slot) * B * N, gsrc + (T - 1 + c * B) * N, bytes,
                  full_g + slot);
+        // warm L2 with the chunks after the ring's depth (no shared memory
+        // needed): their bulk copies then start from L2
+        if constexpr (Cfg::L2A > 0) {
+            const long long cp = c + Cfg::L2A;
+            if (cp < n_chunks) {
+                const long long rp = min(static_cast<long long>(B), n_out_g - cp * B);
+                bulk_prefetch_l2(gsrc + (T - 1 + cp * B) * N, static_cast<uint32_t>(rp * N * sizeof(float2)));
+            }
+        }
     };
     if (producer) {
         for (long long c = 0; c < n_chunks && c < PC; ++c)

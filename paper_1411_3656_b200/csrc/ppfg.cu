@@ -147,10 +147,12 @@ const std::vector<FusedEntry>& fused_table() {
     static const std::vector<FusedEntry> t = {
         // (float4 twiddle tables where they measured faster than float2:
         // C=1024 T=8 FAST 0.86 vs 0.85 at the SKA size, C=512 EXACT 0.68 vs
-        // 0.65, C=64 0.88 vs 0.86, EXACT C=64..256 +2-3 %; three FFT
+        // 0.65, C=64 0.88 vs 0.86, EXACT C=64..256 +2-3 %; L2 prefetch one
+        // chunk ahead at the SKA shape: 2836 vs 2802 GB/s on the 6.5 GB
+        // bench (flat at 1 GiB; -1..2 % on other shapes); three FFT
         // warpgroups at C=128 0.87 vs 0.78, C=256 0.82 vs 0.76, C=512 0.91 vs
         // 0.90 — but not at C=1024 T=4: 0.83 vs 0.86)
-        fused_entry<FusedCfg<10, 8, 2, false, 120, 80, 2, 3, 2, true>>(),
+        fused_entry<FusedCfg<10, 8, 2, false, 120, 80, 2, 3, 2, true, 1>>(),
         fused_entry<FusedCfg<9, 8, 2, false, 120, 80, 2, 3>>(),
         fused_entry<FusedCfg<8, 8, 2, false, 120, 80, 2, 3>>(),
         fused_entry<FusedCfg<7, 8, 2, false, 120, 80, 2, 3>>(),
