@@ -201,6 +201,20 @@ int ppfg_multi_fir_fft(uint64_t n_channels, uint64_t n_taps, const double* coeff
                        uint32_t flags, const int* devices, int n_devices, const void* host_in,
                        uint64_t n_spectra_in, void* host_out);
 
+/* Device-resident stream distributed over GPUs (the halo read from
+ * the peer): segment g holds the next seg_rows[g] input spectra of one stream in
+ * d_in[g], on plans[g]'s device, in a buffer with room for seg_rows[g] +
+ * n_taps - 1 spectra. Each segment's right edge is completed with the first
+ * n_taps - 1 spectra of the following segment(s) by cudaMemcpyPeerAsync over
+ * NVLink/NVSwitch, then the fused FIR+FFT (ppfg_fir_fft) writes out_rows[g] =
+ * (seg_rows[g] + halo) - n_taps + 1 output spectra to d_out[g] — the stream's
+ * outputs in order, byte-identical to one ppfg_fir_fft over the whole stream.
+ * Plans share C and T; one host thread per segment; returns when all are done.
+ * Replaces the multi-worker one-shot of ppf_fir_optimized/channelize_block
+ * (fir.hpp:158-212, dft.hpp:175-235) when the stream is sharded across GPUs. */
+int ppfg_multi_fir_fft_device(const ppfg_plan* plans, int n_segments, void* const* d_in,
+                              const uint64_t* seg_rows, void* const* d_out, uint64_t* out_rows);
+
 /* ---- synthetic input --------------------------------------------- */
 
 /* Counter-based tone + noise: x[n] = e^{2 pi i f n / C} + (g1 + i g2) with

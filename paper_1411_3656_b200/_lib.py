@@ -48,6 +48,8 @@ SIGNATURES = {
                                    C.POINTER(u64), C.POINTER(u64)]),
     "ppfg_multi_fir_fft": (C.c_int, [u64, u64, dp, C.c_uint32, C.POINTER(C.c_int), C.c_int, vp,
                                      u64, vp]),
+    "ppfg_multi_fir_fft_device": (C.c_int, [C.POINTER(vp), C.c_int, C.POINTER(vp), C.POINTER(u64),
+                                            C.POINTER(vp), C.POINTER(u64)]),
     "ppfg_synth": (C.c_int, [u64, u64, u64, u64, vp, C.c_int, C.c_int, vp]),
     "ppfg_generate_prototype": (C.c_int, [u64, u64, C.c_double, C.c_double, dp]),
     "ppfg_flops_for_fir": (u64, [u64, u64, u64]),

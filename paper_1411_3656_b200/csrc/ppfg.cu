@@ -1456,6 +1456,74 @@ int ppfg_multi_fir_fft(uint64_t n_channels, uint64_t n_taps, const double* coeff
     return PPFG_OK;
 }
 
+// Device-resident stream over several GPUs (halo "from peer"):
+// segment g lives in d_in[g] on plans[g]'s device with n_taps - 1 spare rows;
+// its right edge is completed with the first rows of the following
+// segment(s) by cudaMemcpyPeerAsync (NVLink/NVSwitch; a plain device copy when
+// both segments share a device), then the fused FIR+FFT runs on the plan's
+// stream. No collective; one host thread per segment.
+int ppfg_multi_fir_fft_device(const ppfg_plan* plans, int n_segments, void* const* d_in,
+                              const uint64_t* seg_rows, void* const* d_out, uint64_t* out_rows) {
+    if (n_segments < 1 || !plans || !d_in || !seg_rows || !d_out || !out_rows)
+        return fail(PPFG_CONFIG_ERROR, "multi_fir_fft_device: null argument");
+    for (int g = 0; g < n_segments; ++g) {
+        PPFG_TRY(check_plan(plans[g]));
+        if (plans[g]->C != plans[0]->C || plans[g]->T != plans[0]->T || plans[g]->T == 0)
+            return fail(PPFG_CONFIG_ERROR, "multi_fir_fft_device: plans differ in C or T");
+        if (seg_rows[g] && (!d_in[g] || !d_out[g]))
+            return fail(PPFG_CONFIG_ERROR, "multi_fir_fft_device: null segment buffer");
+    }
+    const uint64_t T = plans[0]->T;
+    const uint64_t row_bytes = plans[0]->C * sizeof(float2);
+    std::vector<int> status(n_segments, PPFG_OK);
+    std::vector<std::string> msgs(n_segments);
+    std::vector<std::thread> pool;
+    for (int g = 0; g < n_segments; ++g) {
+        pool.emplace_back([&, g]() {
+            ppfg_plan p = plans[g];
+            DeviceGuard dg(p->device);
+            auto body = [&]() -> int {
+                // halo: the next T-1 rows of the stream, from the following segment(s)
+                uint64_t have = seg_rows[g];
+                uint64_t need = T - 1;
+                for (int k = g + 1; k < n_segments && need > 0; ++k) {
+                    const uint64_t take = std::min<uint64_t>(need, seg_rows[k]);
+                    if (take == 0)
+                        continue;
+                    const int dk = plans[k]->device;
+                    if (dk != p->device) {
+                        const cudaError_t e = cudaDeviceEnablePeerAccess(dk, 0);
+                        if (e == cudaErrorPeerAccessAlreadyEnabled || e == cudaErrorPeerAccessUnsupported)
+                            cudaGetLastError(); // copies still work (staged by the driver)
+                        else if (e != cudaSuccess)
+                            return fail(PPFG_CUDA_ERROR, std::string("peer access: ") + cudaGetErrorString(e));
+                    }
+                    PPFG_CUDA(cudaMemcpyPeerAsync(static_cast<char*>(d_in[g]) + have * row_bytes, p->device,
+                                                  d_in[k], dk, take * row_bytes, p->stream));
+                    have += take;
+                    need -= take;
+                }
+                out_rows[g] = have >= T ? have - T + 1 : 0;
+                if (out_rows[g] == 0)
+                    return PPFG_OK;
+                PPFG_TRY(run(p, Op::FirFft, d_in[g], have, d_out[g], PPFG_MEM_DEVICE, nullptr, T - 1));
+                PPFG_CUDA(cudaStreamSynchronize(p->stream));
+                return PPFG_OK;
+            };
+            const int st = body();
+            if (st != PPFG_OK)
+                msgs[g] = g_err;
+            status[g] = st;
+        });
+    }
+    for (auto& t : pool)
+        t.join();
+    for (int g = 0; g < n_segments; ++g)
+        if (status[g] != PPFG_OK)
+            return fail(status[g], "segment " + std::to_string(g) + ": " + msgs[g]);
+    return PPFG_OK;
+}
+
 // ----------------------------------------------------------------- synth
 int ppfg_synth(uint64_t n_channels, uint64_t seed, uint64_t first_sample, uint64_t n_samples,
                void* out, int mem, int device, void* cuda_stream) {

@@ -491,6 +491,23 @@ def multi_fir_fft(host_in, coeffs: FilterCoefficients, devices, flags=EXACT):
     return out
 
 
+def multi_fir_fft_device(plans, segments, seg_rows, outs):
+    """ppfg_multi_fir_fft_device (halo from the peer): segment g is
+    a CUDA tensor on plans[g]'s device holding seg_rows[g] input spectra plus
+    n_taps - 1 spare rows; returns the output spectra count per segment (outs[g]
+    receives them)."""
+    n = len(plans)
+    if not (len(segments) == len(seg_rows) == len(outs) == n):
+        raise config_error("multi_fir_fft_device: one segment, row count and output per plan")
+    ph = (_lib.vp * n)(*[p._h.value for p in plans])
+    ins = (_lib.vp * n)(*[_Buf(x).ptr for x in segments])
+    os_ = (_lib.vp * n)(*[_Buf(y).ptr for y in outs])
+    rows = (_lib.u64 * n)(*seg_rows)
+    got = (_lib.u64 * n)()
+    _check(_lib.load().ppfg_multi_fir_fft_device(ph, n, ins, rows, os_, got))
+    return [int(v) for v in got]
+
+
 def synth(n_channels, n_samples, seed=1, first_sample=0, out=None, device=0, stream=None):
     """Counter-based tone + noise (ppfg_synth). numpy out -> host generator,
     torch CUDA out -> device kernel; identical bytes."""

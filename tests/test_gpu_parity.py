@@ -367,6 +367,42 @@ def test_shards_reassemble_the_one_shot(cuda, port):
     assert np.array_equal(bits(got), bits(want))
 
 
+# SURVEY §8e halo "from the peer": device segments with spare rows, halos
+# copied from the following segment(s) (cudaMemcpyPeerAsync; on one GPU every
+# segment shares cuda:0, so the copy path is exercised, not NVLink), outputs
+# byte-identical to one ppfg_fir_fft over the stream — including segments
+# shorter than the halo and an empty one.
+@pytest.mark.parametrize("flags", ["exact", "fast"])
+@pytest.mark.parametrize("C,T,rows", [(1024, 8, [3000, 2500, 4001]), (512, 16, [700, 5, 0, 900, 3]),
+                                      (256, 4, [1, 2, 3, 4000])])
+def test_multi_device_segments_with_peer_halo(cuda, C, T, rows, flags):
+    import torch
+    ppf = ppf_mod()
+    S = sum(rows)
+    x = torch.empty((S, C), dtype=torch.complex64, device="cuda")
+    ppf.synth(C, S * C, seed=C + T, out=x)
+    coeffs = ppf.generate_prototype(C, T)
+    f = ppf.EXACT if flags == "exact" else ppf.FAST
+    with ppf.Plan(C, T, coeffs, flags=f) as p:
+        want = p.fir_fft(x)
+    torch.cuda.synchronize()
+    plans = [ppf.Plan(C, T, coeffs, flags=f) for _ in rows]
+    segs, outs, o = [], [], 0
+    for r in rows:
+        seg = torch.zeros((r + T - 1, C), dtype=torch.complex64, device="cuda")
+        seg[:r] = x[o:o + r]
+        segs.append(seg)
+        outs.append(torch.empty((max(r, 1), C), dtype=torch.complex64, device="cuda"))
+        o += r
+    torch.cuda.synchronize()
+    got = ppf.multi_fir_fft_device(plans, segs, rows, outs)
+    for p in plans:
+        p.close()
+    assert sum(got) == S - T + 1
+    cat = torch.cat([outs[g][:got[g]] for g in range(len(rows))])
+    assert torch.equal(cat.view(torch.int64), want.view(torch.int64))
+
+
 def test_host_pipeline_pinned_and_pageable(cuda, port):
     """ppfg_fir_fft with host buffers: multi-chunk double-buffered pipeline,
     pinned (torch pin_memory) and pageable (numpy) inputs give the same bytes."""
