@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
                          long long S_out, long long rows_per_cta, const float* __restrict__ taps,
                          const typename Cfg::TwT* __restrict__ tw_g) {
     constexpr int L = Cfg::L, T = Cfg::T, RLOG = Cfg::RLOG, N = Cfg::N, R = Cfg::R;
-    constexpr int NTG = Cfg::NTG, NFIR = Cfg::NFIR, NFFT = Cfg::NFFT, NT = Cfg::NT;
+    constexpr int NTG = Cfg::NTG, NFIR = Cfg::NFIR, NT = Cfg::NT;
     constexpr int G = Cfg::G, B = Cfg::B;
 
     extern __shared__ __align__(128) unsigned char smem_raw[];

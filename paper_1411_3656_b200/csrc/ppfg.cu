@@ -8,6 +8,7 @@
 #include <cudaTypedefs.h>
 
 #include <atomic>
+#include <condition_variable>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -380,6 +381,74 @@ int ensure_smem_attr(KernelFn fn, size_t smem, int device) {
 
 } // namespace
 
+// Pinned / device buffers and events of the pipelined process_stream, pooled
+// per device across calls and plans (pinning is slow: ~10x a memcpy, and the
+// drop-in creates a plan per process_stream call).
+struct PsBuffers {
+    static constexpr int KH = 3, KD = 2, KO = 3;
+    uint64_t io = 0, rows_cap = 0, taps = 0;
+    void* h_in[KH] = {};
+    void* h_out[KO] = {};
+    void* d_in[KD] = {};
+    void* d_out[KO] = {};
+    cudaEvent_t ev_hin[KH] = {}, ev_din[KD] = {}, ev_comp[KD] = {}, ev_d2h[KO] = {};
+    void release() {
+        for (auto& b : h_in)
+            if (b)
+                cudaFreeHost(b), b = nullptr;
+        for (auto& b : h_out)
+            if (b)
+                cudaFreeHost(b), b = nullptr;
+        for (auto& b : d_in)
+            if (b)
+                cudaFree(b), b = nullptr;
+        for (auto& b : d_out)
+            if (b)
+                cudaFree(b), b = nullptr;
+        for (auto& e : ev_hin)
+            if (e)
+                cudaEventDestroy(e), e = nullptr;
+        for (auto& e : ev_din)
+            if (e)
+                cudaEventDestroy(e), e = nullptr;
+        for (auto& e : ev_comp)
+            if (e)
+                cudaEventDestroy(e), e = nullptr;
+        for (auto& e : ev_d2h)
+            if (e)
+                cudaEventDestroy(e), e = nullptr;
+        io = rows_cap = taps = 0;
+    }
+    // (re)allocate for blocks of io bytes (+ one spectrum of carry) and T taps
+    bool ensure(uint64_t io_, uint64_t row_bytes, uint64_t T) {
+        const uint64_t rows = io_ / row_bytes + 1;
+        if (io >= io_ && rows_cap >= rows && taps == T)
+            return true;
+        release();
+        bool ok = true;
+        for (int i = 0; i < KH && ok; ++i)
+            ok = cudaMallocHost(&h_in[i], io_ + row_bytes) == cudaSuccess &&
+                 cudaEventCreateWithFlags(&ev_hin[i], cudaEventDisableTiming) == cudaSuccess;
+        for (int i = 0; i < KO && ok; ++i)
+            ok = cudaMallocHost(&h_out[i], rows * row_bytes) == cudaSuccess &&
+                 cudaMalloc(&d_out[i], rows * row_bytes) == cudaSuccess &&
+                 cudaEventCreateWithFlags(&ev_d2h[i], cudaEventDisableTiming) == cudaSuccess;
+        for (int i = 0; i < KD && ok; ++i)
+            ok = cudaMalloc(&d_in[i], (T - 1 + rows) * row_bytes) == cudaSuccess &&
+                 cudaEventCreateWithFlags(&ev_din[i], cudaEventDisableTiming) == cudaSuccess &&
+                 cudaEventCreateWithFlags(&ev_comp[i], cudaEventDisableTiming) == cudaSuccess;
+        if (!ok) {
+            release();
+            cudaGetLastError();
+            return false;
+        }
+        io = io_;
+        rows_cap = rows;
+        taps = T;
+        return true;
+    }
+};
+
 // ================================================================== plans
 struct ppfg_plan_s {
     int device = 0;
@@ -411,6 +480,30 @@ struct ppfg_plan_s {
     void* d_bins = nullptr; // bins of the unfused detection path
     size_t bins_bytes = 0;
 };
+
+// Process-wide pool of PsBuffers per device, kept until exit like a caching
+// allocator: concurrent streams each take their own, idle ones are reused.
+struct PsPool {
+    std::mutex mu;
+    std::map<int, std::vector<PsBuffers*>> idle;
+    PsBuffers* acquire(int device) {
+        std::lock_guard<std::mutex> lk(mu);
+        auto& v = idle[device];
+        if (v.empty())
+            return new PsBuffers();
+        PsBuffers* b = v.back();
+        v.pop_back();
+        return b;
+    }
+    void give_back(int device, PsBuffers* b) {
+        std::lock_guard<std::mutex> lk(mu);
+        idle[device].push_back(b);
+    }
+};
+PsPool& ps_pool() {
+    static PsPool* pool = new PsPool(); // never destroyed: no teardown-order issues at exit
+    return *pool;
+}
 
 namespace {
 
@@ -1272,6 +1365,7 @@ int ppfg_plan_destroy(ppfg_plan p) {
     cudaFree(p->d_ones);
     cudaFree(p->d_part);
     cudaFree(p->d_bins);
+
     for (int i = 0; i < 2; ++i) {
         cudaFree(p->d_in[i]);
         cudaFree(p->d_out[i]);
@@ -1632,6 +1726,328 @@ int ppfg_generate_prototype(uint64_t n_channels, uint64_t n_taps, double beta,
 // of newly completed spectra is uploaded right behind it, the fused kernel
 // runs over history ++ chunk, and the last T-1 spectra become the next history
 // (ping-pong buffers, no overlap hazards).
+// ---------------------------------------------------- pipelined process_stream
+// ppfg_process_stream as three concurrent stages (SURVEY §8d host-streamed
+// mode): a reader thread pulls blocks of block_spectra*C*8 bytes through the
+// read callback into pinned slots (the partial spectrum at a block's end is
+// carried into the next slot's prefix); this thread copies each block's whole
+// spectra H2D behind the device-resident history (stream s_h2d), runs the fused
+// FIR+FFT (plan stream) and copies the spectra back into pinned output slots
+// (s_d2h); a writer thread hands them to the write callback in order. Reading,
+// PCIe and writing overlap instead of alternating. Byte-identical to the
+// reference's loop (pipeline.hpp:89-200): outputs do not depend on the block
+// partition, and the byte / sample carry, decode offsets, zero_prime and
+// dropped_samples are the same.
+namespace {
+
+struct PsShared {
+    std::mutex mu;
+    std::condition_variable cv;
+    bool stop = false; // any stage failed
+    int status = PPFG_OK;
+    std::string msg;
+    uint64_t err_offset = 0;
+    void fail_with(int st, const std::string& m, uint64_t off = 0) {
+        std::lock_guard<std::mutex> lk(mu);
+        if (status == PPFG_OK) {
+            status = st;
+            msg = m;
+            err_offset = off;
+        }
+        stop = true;
+        cv.notify_all();
+    }
+};
+
+struct PsBlock {
+    uint64_t full = 0; // whole spectra in the slot
+    int slot = 0;
+    bool end = false;
+};
+
+int process_stream_pipelined(ppfg_plan p, uint64_t block_spectra, int zero_prime, int fft_fallback,
+                             ppfg_read_fn read, void* read_ctx, ppfg_write_fn write, void* write_ctx,
+                             ppfg_stream_state* state) {
+    constexpr int KH = PsBuffers::KH, KD = PsBuffers::KD, KO = PsBuffers::KO;
+    const uint64_t C = p->C, T = p->T;
+    const uint64_t row_bytes = C * sizeof(float2);
+    if (T == 0)
+        return fail(PPFG_CONFIG_ERROR, "config: n_taps must be >= 1");
+    if (block_spectra < T) // PpfConfig::validate, pipeline.hpp:33-34
+        return fail(PPFG_CONFIG_ERROR, "config: block_spectra must be >= n_taps");
+    const uint64_t io = block_spectra * row_bytes; // pipeline.hpp:113
+    DeviceGuard dg(p->device);
+
+    PsBuffers* bufs = ps_pool().acquire(p->device);
+    struct GiveBack {
+        int dev;
+        PsBuffers* b;
+        ~GiveBack() { ps_pool().give_back(dev, b); }
+    } give_back{p->device, bufs};
+    if (!bufs->ensure(io, row_bytes, T))
+        return fail(PPFG_CUDA_ERROR, "process_stream: buffer allocation failed");
+    void* const* h_in = bufs->h_in;
+    void* const* h_out = bufs->h_out;
+    void* const* d_in = bufs->d_in;
+    void* const* d_out = bufs->d_out;
+    cudaEvent_t* ev_hin = bufs->ev_hin;
+    cudaEvent_t* ev_din = bufs->ev_din;
+    cudaEvent_t* ev_comp = bufs->ev_comp;
+    cudaEvent_t* ev_d2h = bufs->ev_d2h;
+
+    PsShared sh;
+    // reader -> GPU queue (bounded by the KH host slots)
+    std::vector<PsBlock> rq;
+    size_t rq_head = 0;
+    std::vector<uint64_t> hin_released(KH, 0); // blocks whose use of the slot ended
+    std::vector<bool> hin_event(KH, false);    // ... with an H2D to wait for
+    uint64_t final_carry = 0, final_offset = 0;
+    bool read_error = false;
+    uint64_t read_error_offset = 0;
+
+    std::thread reader([&]() {
+        DeviceGuard rdg(p->device);
+        uint64_t carry = 0, offset = 0;
+        int prev = -1;
+        uint64_t prev_full = 0;
+        for (uint64_t blk = 0;; ++blk) {
+            const int h = static_cast<int>(blk % KH);
+            bool need_sync = false;
+            {
+                std::unique_lock<std::mutex> lk(sh.mu);
+                sh.cv.wait(lk, [&] { return sh.stop || hin_released[h] >= blk / KH; });
+                if (sh.stop)
+                    return;
+                need_sync = blk >= KH && hin_event[h];
+            }
+            if (need_sync && cudaEventSynchronize(ev_hin[h]) != cudaSuccess) {
+                sh.fail_with(PPFG_CUDA_ERROR, "process_stream: H2D failed");
+                return;
+            }
+            char* slot = static_cast<char*>(h_in[h]);
+            if (carry)
+                std::memcpy(slot, static_cast<char*>(h_in[prev]) + prev_full * row_bytes, carry);
+            const int64_t got = read(read_ctx, slot + carry, io);
+            bool end = false;
+            PsBlock b;
+            b.slot = h;
+            if (got < 0) { // pipeline.hpp:141-143
+                std::lock_guard<std::mutex> lk(sh.mu);
+                read_error = true;
+                read_error_offset = offset;
+                end = true;
+            } else if (got == 0) {
+                end = true;
+            } else {
+                offset += static_cast<uint64_t>(got);
+                const uint64_t total = carry + static_cast<uint64_t>(got);
+                b.full = total / row_bytes;
+                carry = total % row_bytes;
+                prev = h;
+                prev_full = b.full;
+                if (static_cast<uint64_t>(got) < io) // short read: end of stream (source.eof())
+                    end = true;
+            }
+            std::lock_guard<std::mutex> lk(sh.mu);
+            if (!read_error && got > 0)
+                rq.push_back(b);
+            if (end) {
+                final_carry = carry;
+                final_offset = offset;
+                PsBlock e;
+                e.end = true;
+                rq.push_back(e);
+                sh.cv.notify_all();
+                return;
+            }
+            sh.cv.notify_all();
+        }
+    });
+
+    // GPU -> writer queue (bounded by the KO output slots)
+    struct WItem {
+        int o;
+        uint64_t bytes;
+        bool end;
+    };
+    std::vector<WItem> wq;
+    size_t wq_head = 0;
+    std::vector<uint64_t> out_released(KO, 0);
+    std::thread writer([&]() {
+        DeviceGuard wdg(p->device);
+        for (;;) {
+            WItem it;
+            {
+                std::unique_lock<std::mutex> lk(sh.mu);
+                sh.cv.wait(lk, [&] { return sh.stop || wq_head < wq.size(); });
+                if (wq_head >= wq.size())
+                    return; // stopped
+                it = wq[wq_head++];
+            }
+            if (it.end)
+                return;
+            if (cudaEventSynchronize(ev_d2h[it.o]) != cudaSuccess) {
+                sh.fail_with(PPFG_CUDA_ERROR, "process_stream: D2H failed");
+                return;
+            }
+            if (it.bytes && write(write_ctx, h_out[it.o], it.bytes) != 0) {
+                sh.fail_with(PPFG_IO_ERROR, "process_stream: sink write failed");
+                return;
+            }
+            std::lock_guard<std::mutex> lk(sh.mu);
+            ++out_released[it.o];
+            sh.cv.notify_all();
+        }
+    });
+
+    ppfg_stream_state st{};
+    cudaStream_t s_h2d = p->s_h2d, s_comp = p->stream, s_d2h = p->s_d2h;
+    uint64_t hist = 0;
+    if (zero_prime && T > 1) { // pipeline.hpp:110-111
+        hist = T - 1;
+        cudaMemsetAsync(d_in[0], 0, hist * row_bytes, s_h2d);
+    }
+    const bool pow2 = is_pow2(C);
+    int prev_d = -1;
+    uint64_t prev_total = 0, k = 0;
+    auto gpu_fail = [&](int rc) {
+        sh.fail_with(rc, g_err.empty() ? std::string("process_stream: CUDA error") : g_err, g_err_offset);
+    };
+    for (;;) {
+        PsBlock b;
+        {
+            std::unique_lock<std::mutex> lk(sh.mu);
+            sh.cv.wait(lk, [&] { return sh.stop || rq_head < rq.size(); });
+            if (sh.stop)
+                break;
+            b = rq[rq_head++];
+        }
+        if (b.end)
+            break;
+        const int h = b.slot;
+        if (b.full == 0) { // nothing whole yet: the carry moves on (pipeline.hpp:177)
+            std::lock_guard<std::mutex> lk(sh.mu);
+            hin_event[h] = false;
+            ++hin_released[h];
+            sh.cv.notify_all();
+            continue;
+        }
+        const int d = static_cast<int>(k % KD), o = static_cast<int>(k % KO);
+        const uint64_t total = hist + b.full;
+        int rc = PPFG_OK;
+        // input: slot d is free once block k-KD's kernel has read it
+        if (k >= KD && cudaStreamWaitEvent(s_h2d, ev_comp[d], 0) != cudaSuccess)
+            rc = fail(PPFG_CUDA_ERROR, "process_stream: stream wait failed");
+        if (rc == PPFG_OK && hist && prev_d >= 0 && prev_d != d)
+            rc = cudaMemcpyAsync(d_in[d], static_cast<char*>(d_in[prev_d]) + (prev_total - hist) * row_bytes,
+                                 hist * row_bytes, cudaMemcpyDeviceToDevice, s_h2d) == cudaSuccess
+                     ? PPFG_OK
+                     : fail(PPFG_CUDA_ERROR, "process_stream: history copy failed");
+        if (rc == PPFG_OK)
+            rc = cudaMemcpyAsync(static_cast<char*>(d_in[d]) + hist * row_bytes, h_in[h], b.full * row_bytes,
+                                 cudaMemcpyHostToDevice, s_h2d) == cudaSuccess &&
+                         cudaEventRecord(ev_hin[h], s_h2d) == cudaSuccess &&
+                         cudaEventRecord(ev_din[d], s_h2d) == cudaSuccess
+                     ? PPFG_OK
+                     : fail(PPFG_CUDA_ERROR, "process_stream: H2D failed");
+        {
+            std::lock_guard<std::mutex> lk(sh.mu);
+            hin_event[h] = true;
+            ++hin_released[h];
+            sh.cv.notify_all();
+        }
+        st.bytes_in += b.full * row_bytes;
+        const uint64_t n_out = total >= T ? total - T + 1 : 0;
+        if (rc == PPFG_OK && n_out) {
+            if (!fft_fallback && !pow2)
+                rc = fail(PPFG_UNSUPPORTED_SIZE,
+                          "channelize_block: non-power-of-two channel count with fallback disabled");
+            // output slot o: its previous D2H has been written out by the writer
+            if (rc == PPFG_OK) {
+                std::unique_lock<std::mutex> lk(sh.mu);
+                sh.cv.wait(lk, [&] { return sh.stop || out_released[o] >= k / KO; });
+                if (sh.stop)
+                    break;
+            }
+            if (rc == PPFG_OK && (cudaStreamWaitEvent(s_comp, ev_din[d], 0) != cudaSuccess ||
+                                  (k >= KO && cudaStreamWaitEvent(s_comp, ev_d2h[o], 0) != cudaSuccess)))
+                rc = fail(PPFG_CUDA_ERROR, "process_stream: stream wait failed");
+            if (rc == PPFG_OK)
+                rc = launch_fir_fft(p, static_cast<const float2*>(d_in[d]), total,
+                                    static_cast<float2*>(d_out[o]), s_comp);
+            if (rc == PPFG_OK &&
+                (cudaEventRecord(ev_comp[d], s_comp) != cudaSuccess ||
+                 cudaStreamWaitEvent(s_d2h, ev_comp[d], 0) != cudaSuccess ||
+                 cudaMemcpyAsync(h_out[o], d_out[o], n_out * row_bytes, cudaMemcpyDeviceToHost, s_d2h) !=
+                     cudaSuccess ||
+                 cudaEventRecord(ev_d2h[o], s_d2h) != cudaSuccess))
+                rc = fail(PPFG_CUDA_ERROR, "process_stream: D2H failed");
+            if (rc == PPFG_OK) {
+                std::lock_guard<std::mutex> lk(sh.mu);
+                wq.push_back({o, n_out * row_bytes, false});
+                sh.cv.notify_all();
+            }
+        } else if (rc == PPFG_OK) {
+            // no output: the slot is still read by the next block's history copy
+            // (same stream) and must not be refilled before this block's H2D
+            if (cudaEventRecord(ev_comp[d], s_h2d) != cudaSuccess)
+                rc = fail(PPFG_CUDA_ERROR, "process_stream: event record failed");
+            std::lock_guard<std::mutex> lk(sh.mu);
+            ++out_released[o]; // slot o unused by this block
+            sh.cv.notify_all();
+        }
+        if (rc != PPFG_OK) {
+            gpu_fail(rc);
+            break;
+        }
+        st.spectra_processed += n_out;
+        st.bytes_out += n_out * row_bytes;
+        hist = std::min<uint64_t>(T - 1, total); // carry_history (pipeline.hpp:55-73)
+        prev_d = d;
+        prev_total = total;
+        ++k;
+    }
+    {
+        std::lock_guard<std::mutex> lk(sh.mu);
+        wq.push_back({0, 0, true});
+        sh.cv.notify_all();
+    }
+    writer.join();
+    {
+        std::lock_guard<std::mutex> lk(sh.mu);
+        sh.stop = true; // release a reader still waiting for a slot
+        sh.cv.notify_all();
+    }
+    reader.join();
+    cudaStreamSynchronize(s_h2d);
+    cudaStreamSynchronize(s_comp);
+    cudaStreamSynchronize(s_d2h);
+    int rc = sh.status;
+    std::string msg = sh.msg;
+    uint64_t off = sh.err_offset;
+    if (rc == PPFG_OK && read_error) { // pipeline.hpp:141-143
+        rc = PPFG_DECODE_ERROR;
+        off = read_error_offset;
+        msg = "process_stream: source read failed at byte offset " + std::to_string(off);
+    }
+    if (rc == PPFG_OK && final_carry % 8 != 0) { // pipeline.hpp:190-192
+        rc = PPFG_DECODE_ERROR;
+        off = final_offset - final_carry % 8;
+        msg = "process_stream: stream truncated mid-sample at byte offset " + std::to_string(off);
+    }
+    if (rc == PPFG_OK)
+        st.dropped_samples += final_carry / 8; // pipeline.hpp:194
+    if (state)
+        *state = st;
+    if (rc != PPFG_OK) {
+        g_err_offset = off;
+        return fail(rc, msg);
+    }
+    return PPFG_OK;
+}
+
+} // namespace
+
 struct ppfg_stream_s {
     ppfg_plan plan = nullptr;
     uint64_t block_spectra = 0;
@@ -1799,41 +2215,8 @@ int ppfg_process_stream(ppfg_plan p, uint64_t block_spectra, int zero_prime, int
     PPFG_TRY(check_plan(p));
     if (!read || !write)
         return fail(PPFG_CONFIG_ERROR, "process_stream: null callback");
-    ppfg_stream s = nullptr;
-    PPFG_TRY(ppfg_stream_open(&s, p, block_spectra, zero_prime, fft_fallback));
-    const uint64_t row_bytes = p->C * 8;
-    const uint64_t io = block_spectra * row_bytes; // pipeline.hpp:113
-    std::vector<char> in(io);
-    std::vector<char> outb((block_spectra + 2) * row_bytes + row_bytes);
-    int rc = PPFG_OK;
-    for (;;) {
-        const int64_t got = read(read_ctx, in.data(), io);
-        if (got < 0) {
-            g_err_offset = s->stream_offset;
-            rc = fail(PPFG_DECODE_ERROR, "process_stream: source read failed at byte offset " +
-                                             std::to_string(s->stream_offset));
-            break;
-        }
-        if (got == 0)
-            break;
-        uint64_t out_len = 0;
-        rc = ppfg_stream_push(s, in.data(), static_cast<uint64_t>(got), outb.data(), outb.size(),
-                              &out_len);
-        if (rc != PPFG_OK)
-            break;
-        if (out_len && write(write_ctx, outb.data(), out_len) != 0) {
-            rc = fail(PPFG_IO_ERROR, "process_stream: sink write failed");
-            break;
-        }
-        if (static_cast<uint64_t>(got) < io)
-            break;
-    }
-    if (rc == PPFG_OK)
-        rc = ppfg_stream_close(s, state);
-    else if (state)
-        *state = s->st;
-    ppfg_stream_destroy(s);
-    return rc;
+    return process_stream_pipelined(p, block_spectra, zero_prime, fft_fallback, read, read_ctx, write,
+                                    write_ctx, state);
 }
 
 } // extern "C"
