@@ -90,3 +90,20 @@ def test_synth_host_is_deterministic_and_tone_plus_noise():
     noise = a - np.exp(2j * np.pi * (C / 8 + 0.3) * np.arange(4096) / C).astype(np.complex64)
     assert abs(noise.real.std() - 1.0) < 0.05 and abs(noise.imag.std() - 1.0) < 0.05
     assert abs(noise.mean()) < 0.05
+
+
+def test_new_entry_points_validate_arguments_without_a_gpu():
+    """ppfg_multi_fir_fft_device and ppfg_process_stream reject null arguments
+    before touching a device (status codes of include/ppfg.h)."""
+    import ctypes as C
+    from paper_1411_3656_b200 import _lib
+    lib = _lib.load()
+    CONFIG_ERROR = 1   # PPFG_CONFIG_ERROR
+    rows = (C.c_uint64 * 1)(8)
+    got = (C.c_uint64 * 1)()
+    assert lib.ppfg_multi_fir_fft_device(None, 1, None, rows, None, got) == CONFIG_ERROR
+    assert lib.ppfg_multi_fir_fft_device(None, 0, None, None, None, None) == CONFIG_ERROR
+    assert b"null" in lib.ppfg_last_error()
+    st = _lib.StreamState()
+    assert lib.ppfg_process_stream(None, 4096, 0, 1, _lib.READ_FN(0), None, _lib.WRITE_FN(0), None,
+                                   C.byref(st)) == CONFIG_ERROR
