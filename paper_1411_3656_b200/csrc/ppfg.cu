@@ -2128,24 +2128,38 @@ int ppfg_stream_push(ppfg_stream s, const void* bytes, uint64_t n, void* out, ui
             s->byte_carry_n = 0;
         }
     }
-    const uint64_t full = avail / 8, tail = avail % 8;
-    const size_t old = s->sample_carry.size();
-    s->sample_carry.resize(old + full);
-    std::memcpy(s->sample_carry.data() + old, data, full * 8);
-    if (tail) {
-        std::memcpy(s->byte_carry, data + full * 8, tail);
-        s->byte_carry_n = static_cast<int>(tail);
-    }
+    // append bytes to the sample / byte carry (pipeline.hpp:165-172)
+    auto carry_bytes = [&](const uint8_t* d, uint64_t k) {
+        const uint64_t full = k / 8, tail = k % 8;
+        const size_t old = s->sample_carry.size();
+        s->sample_carry.resize(old + full);
+        std::memcpy(s->sample_carry.data() + old, d, full * 8);
+        if (tail) {
+            std::memcpy(s->byte_carry, d + full * 8, tail);
+            s->byte_carry_n = static_cast<int>(tail);
+        }
+    };
     s->stream_offset += n;
-
-    const uint64_t full_spectra = s->sample_carry.size() / C;
+    // nothing carried: whole spectra go to the device straight from the
+    // caller's buffer (a DMA when it is pinned), only the tail is carried
+    const bool direct = s->sample_carry.empty() && s->byte_carry_n == 0;
+    const float2* src;
+    uint64_t full_spectra;
+    if (direct) {
+        full_spectra = avail / row_bytes;
+        src = reinterpret_cast<const float2*>(data);
+    } else {
+        carry_bytes(data, avail);
+        full_spectra = s->sample_carry.size() / C;
+        src = s->sample_carry.data();
+    }
     uint64_t done = 0;
     char* o = static_cast<char*>(out);
     while (done < full_spectra) {
         const uint64_t rows = std::min(s->cap_rows, full_spectra - done);
         float2* buf = s->d_buf[s->cur];
-        PPFG_CUDA(cudaMemcpyAsync(buf + s->hist_rows * C, s->sample_carry.data() + done * C,
-                                  rows * row_bytes, cudaMemcpyHostToDevice, p->stream));
+        PPFG_CUDA(cudaMemcpyAsync(buf + s->hist_rows * C, src + done * C, rows * row_bytes,
+                                  cudaMemcpyHostToDevice, p->stream));
         const uint64_t total = s->hist_rows + rows;
         s->st.bytes_in += rows * row_bytes;
         if (total >= T) {
@@ -2172,8 +2186,11 @@ int ppfg_stream_push(ppfg_stream s, const void* bytes, uint64_t n, void* out, ui
         s->hist_rows = keep;
         done += rows;
     }
-    s->sample_carry.erase(s->sample_carry.begin(),
-                          s->sample_carry.begin() + static_cast<std::ptrdiff_t>(done * C));
+    if (direct)
+        carry_bytes(data + full_spectra * row_bytes, avail - full_spectra * row_bytes);
+    else
+        s->sample_carry.erase(s->sample_carry.begin(),
+                              s->sample_carry.begin() + static_cast<std::ptrdiff_t>(done * C));
     PPFG_CUDA(cudaStreamSynchronize(p->stream));
     return PPFG_OK;
 }
