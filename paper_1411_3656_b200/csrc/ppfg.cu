@@ -152,19 +152,21 @@ const std::vector<FusedEntry>& fused_table() {
         // chunk ahead at the SKA shape: 2836 vs 2802 GB/s on the 6.5 GB
         // bench (flat at 1 GiB; -1..2 % on other shapes); three FFT
         // warpgroups at C=128 0.87 vs 0.78, C=256 0.82 vs 0.76, C=512 0.91 vs
-        // 0.90 — but not at C=1024 T=4: 0.83 vs 0.86)
+        // 0.90 — but not at C=1024 T=4: 0.83 vs 0.86; FIR/FFT registers
+        // 136/120 instead of 160/96 at C=512 T=16 0.76 vs 0.72 and FP64
+        // C=1024 T=4 0.762 vs 0.753)
         fused_entry<FusedCfg<10, 8, 2, false, 120, 80, 2, 3, 2, true, 1>>(),
         fused_entry<FusedCfg<9, 8, 2, false, 120, 80, 2, 3>>(),
         fused_entry<FusedCfg<8, 8, 2, false, 120, 80, 2, 3>>(),
         fused_entry<FusedCfg<7, 8, 2, false, 120, 80, 2, 3>>(),
         fused_entry<FusedCfg<6, 8, 1, false, 120, 80, 2, 3, 2, true>>(),
         fused_entry<FusedCfg<10, 4, 2, false>>(),
-        fused_entry<FusedCfg<9, 16, 1, false>>(),
+        fused_entry<FusedCfg<9, 16, 1, false, 136, 120>>(),
         fused_entry<FusedCfg<9, 8, 1, true, 160, 96, 4, 2, 2, true>>(),
         fused_entry<FusedCfg<8, 8, 1, true, 160, 96, 4, 2, 2, true>>(),
         fused_entry<FusedCfg<7, 8, 1, true, 160, 96, 4, 2, 2, true>>(),
         fused_entry<FusedCfg<6, 8, 1, true, 160, 96, 4, 2, 2, true>>(),
-        fused_entry<FusedCfg<10, 4, 2, true>>(),
+        fused_entry<FusedCfg<10, 4, 2, true, 136, 120>>(),
         // small C at T = 4 and 16 (register budget: 3T·R FP32, 6T·R FP64 per FIR thread)
         fused_entry<FusedCfg<8, 16, 1, false>>(),
         fused_entry<FusedCfg<7, 16, 1, false>>(),
