@@ -209,10 +209,13 @@ const std::vector<FusedEntry>& fused_table() {
         // 0.47 vs 0.44; FAST C=2048/4096 gained 15-27 % from float2)
         // (T=32 FAST: the unfused K1b FP32 FIR -> FFT measured 0.43 vs 0.42;
         // FIR/FFT registers 136/120 instead of 152/104 at FAST C=1024 T=16
-        // 0.645 vs 0.619 and C=2048 0.688 vs 0.624 — not at C=4096 or FP64)
+        // 0.645 vs 0.619 and C=2048 0.688 vs 0.624 — not at C=4096 or FP64 C=2048;
+        // FP64 C=1024 T=8 with float4 twiddles 0.629 vs 0.620 over four A/B
+        // pairs; 4-CTA clusters 0.51, W=4 passes 0.44, FIR 168/88 0.44)
+
         split_entry<SplitCfg<10, 1, 16, false, 2, 5, 136, 120, 0, true>>(true),
         split_entry<SplitCfg<10, 2, 32, false, 2, 5, 152, 104, 0, true>>(false),
-        split_entry<SplitCfg<10, 1, 8, true>>(true),
+        split_entry<SplitCfg<10, 1, 8, true, 2, 5, 136, 120, 0, true>>(true),
         split_entry<SplitCfg<10, 2, 16, true, 2, 5, 152, 104, 0, true>>(true),
         split_entry<SplitCfg<11, 1, 8, false, 2, 5, 136, 120>>(true),
         split_entry<SplitCfg<11, 2, 8, true, 2, 5, 152, 104, 0, true>>(true),
