@@ -211,7 +211,10 @@ const std::vector<FusedEntry>& fused_table() {
         // FIR/FFT registers 136/120 instead of 152/104 at FAST C=1024 T=16
         // 0.645 vs 0.619 and C=2048 0.688 vs 0.624 — not at C=4096 or FP64 C=2048;
         // FP64 C=1024 T=8 with float4 twiddles 0.629 vs 0.620 over four A/B
-        // pairs; 4-CTA clusters 0.51, W=4 passes 0.44, FIR 168/88 0.44)
+        // pairs; 4-CTA clusters 0.51, W=4 passes 0.44, FIR 168/88 0.44.
+        // Rejected in the same A/B: FAST C=4096 float4 0.42 / 8-CTA 0.31 vs
+        // 0.53; FP64 T=16 168/88 0.402 vs 0.403; FAST T=32 cluster 136/120
+        // 0.41, 168/88 0.42, 8-CTA 0.28 — all below unfused K1b 0.43)
 
         split_entry<SplitCfg<10, 1, 16, false, 2, 5, 136, 120, 0, true>>(true),
         split_entry<SplitCfg<10, 2, 32, false, 2, 5, 152, 104, 0, true>>(false),

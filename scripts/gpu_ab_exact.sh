@@ -1,5 +1,6 @@
-# A/B of register/cluster variants of the EXACT C=1024 T=8 cluster entry (build/libppfg_V.so from build_variant.sh)
+# A/B of register/cluster/twiddle variants of cluster entries (build/libppfg_V.so from build_variant.sh)
 mkdir -p gpurun_out
-P="1024:8:exact" bash scripts/gpu_variants.sh "r136tw4 q4 q4r152 w4" > gpurun_out/ab1.log 2>&1
-P="1024:8:exact" bash scripts/gpu_variants.sh "r136tw4 q4 q4r152 w4" >> gpurun_out/ab1.log 2>&1
+for i in 1 2; do
+P="1024:32:fast-cluster 1024:32:fast" bash scripts/gpu_variants.sh "t32r136 t32r168 t32q8" >> gpurun_out/ab1.log 2>&1
+done
 cat gpurun_out/ab1.log
