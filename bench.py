@@ -19,9 +19,22 @@ over ranks of the device-timed region.
           ppfg_fir_fft's chunked double-buffered pipeline.
 `roofline` the dominant (only) kernel: algorithmic bytes 8*C*(S_in+S_out) per
           launch / mean launch time vs the measured HBM copy peak.
+`exact`   the same step in the reference's own precision (FP64 FIR
+          accumulation, bit-identical to ppf_fir_optimized -> channelize_block):
+          CUDA-event time, roofline fraction, and a bitwise check of its whole
+          output.
+`parity`  the WHOLE timed output (every spectrum of rank 0's shard) against the
+          reference's CPU implementation (oracle/_ref: ppf_fir_optimized ->
+          channelize_block, fir.hpp:158-212 / dft.hpp:175-235, all host cores),
+          in chunks: FAST max|d|/RMS (north star bar 1e-5*log2 C), EXACT bitwise.
 `cpu_baseline` the reference's own CPU compute pass (oracle/_ref: carry_history
           -> ppf_fir_optimized -> channelize_block, bench.hpp:129-150) on all
-          host cores, on a bounded 1 GiB sample, rank 0 at N=1 only.
+          host cores and on one, plus ppf_fir_optimized alone, on bounded
+          samples, rank 0 at N=1 only.
+
+The reference arm (--impl reference) loads nothing from paper_1411_3656_b200:
+coefficients come from the reference's own generate_prototype and the input
+from the oracle's copy of the synthetic generator (oracle/ppf_oracle.c).
 """
 from __future__ import annotations
 
@@ -134,12 +147,21 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_reference_sample(C, T, coeffs, sample_spectra, reps, workers):
     """Time the reference's own CPU compute pass (bench.hpp:129-150) on a bounded
     sample of the same workload. Returns (GB/s of input, kind, cores, seconds)."""
     import oracle
-    from paper_1411_3656_b200 import ppf
-    x = ppf.synth(C, sample_spectra * C, seed=1)
+    x = oracle.port().synth(C, sample_spectra * C, seed=1)
     ref = oracle.reference()
     if ref is not None:
         secs, emitted = ref.compute_pass(x, C, T, coeffs, block_spectra=4096, workers=workers,
@@ -158,19 +180,37 @@ def cpu_reference_sample(C, T, coeffs, sample_spectra, reps, workers):
     return sample_spectra * C * 8 / t / 1e9, kind, cores, secs
 
 
+def cpu_fir_alone(C, T, coeffs, sample_spectra, reps, workers):
+    """ppf_fir_optimized alone (fir.hpp:158-212), one-shot on a bounded sample,
+    best of `reps`: GB/s of input."""
+    import oracle
+    ref = oracle.reference()
+    if ref is None:
+        return None
+    x = oracle.port().synth(C, sample_spectra * C, seed=1)
+    best = None
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        ref.fir(x, C, T, coeffs, reference=False, workers=workers)
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    return sample_spectra * C * 8 / best / 1e9
+
+
 def run_reference_arm(args, rank, world):
     """--impl reference: the reference's CPU implementation of the path on this
-    box's host cores (oracle/_ref), rank 0 only."""
+    box's host cores (oracle/_ref), rank 0 only. Nothing of the product
+    (paper_1411_3656_b200 / libppfg.so) is loaded on this arm."""
     if rank != 0:
         return
     C, T, S_in, desc = CONFIGS[args.config]
-    from paper_1411_3656_b200 import ppf
-    coeffs = ppf.generate_prototype(C, T).values
-    workers = os.cpu_count() or 1
-    sample = max(T, (args.cpu_sample_mib << 20) // (C * 8))
     import oracle
     ref = oracle.reference()
-    x = ppf.synth(C, sample * C, seed=1)
+    coeffs = ref.generate_prototype(C, T) if ref is not None else \
+        oracle.port().generate_prototype(C, T)           # coeff.hpp:110-144
+    workers = os.cpu_count() or 1
+    sample = max(T, (args.cpu_sample_mib << 20) // (C * 8))
+    x = oracle.port().synth(C, sample * C, seed=1)
     step_times = []
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
@@ -194,12 +234,59 @@ def run_reference_arm(args, rank, world):
         "config": {"workload": desc, "n_channels": C, "n_taps": T,
                    "sample_spectra": sample, "sample_bytes": sample * C * 8},
         "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": cores, "kind": kind,
+                         "cpu_model": cpu_model(),
                          "sample": f"{sample} spectra ({sample * C * 8 / 2**20:.0f} MiB) of the "
                                    f"{args.config} workload per step, compute pass with "
                                    f"block_spectra=4096, workers={cores}"},
         "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def full_parity(x, outputs, C, T, coeffs, chunk_rows):
+    """Compare every output spectrum of the timed run with the reference's CPU
+    implementation (oracle/_ref ppf_fir_optimized -> channelize_block, all host
+    cores; the oracle port if the reference was not built), chunk by chunk.
+    outputs: {"fast": y, "exact": y2, ...} device tensors [S_out, C] complex64.
+    Returns {name: {...}} with max|d|/RMS over all outputs and, for exact
+    modes, the count of outputs whose bits differ."""
+    import torch
+    import oracle
+    ref = oracle.reference()
+    workers = os.cpu_count() or 1
+    S_out = next(iter(outputs.values())).shape[0]
+    acc = {k: {"maxd": 0.0, "mism": 0} for k in outputs}
+    sumsq = 0.0
+    t0 = time.perf_counter()
+    for o in range(0, S_out, chunk_rows):
+        n = min(chunk_rows, S_out - o)
+        xin = x[o:o + n + T - 1].cpu().numpy()
+        if ref is not None:
+            want = ref.fir_fft(xin, C, T, coeffs, workers=workers)
+        else:
+            want = oracle.port().fir_fft(xin, C, T, coeffs)
+        wd = torch.from_numpy(want.view(np.complex64).reshape(n, C)).to(x.device)
+        w64 = wd.to(torch.complex128)
+        sumsq += float((w64.real ** 2 + w64.imag ** 2).sum())
+        for k, y in outputs.items():
+            yk = y[o:o + n]
+            acc[k]["maxd"] = max(acc[k]["maxd"], float((yk.to(torch.complex128) - w64).abs().max()))
+            acc[k]["mism"] += int((torch.view_as_real(yk).view(torch.int32) !=
+                                   torch.view_as_real(wd).view(torch.int32)).any(-1).sum())
+        del wd, w64
+    rms = (sumsq / (S_out * C)) ** 0.5
+    out = {}
+    for k, a in acc.items():
+        out[k] = {"n_outputs": S_out * C, "max_err_over_rms": a["maxd"] / rms if rms else a["maxd"],
+                  "outputs_not_bit_identical": a["mism"],
+                  "bit_identical": a["mism"] == 0,
+                  "tolerance": 1e-5 * float(np.log2(C)) if C > 1 else 1e-6,
+                  "checker": ("oracle/_ref (the reference compiled from its sources, "
+                              f"ppf_fir_optimized -> channelize_block, workers={workers})")
+                  if ref is not None else "oracle port (C restatement, 1 thread)"}
+        out[k]["pass"] = bool(out[k]["max_err_over_rms"] <= out[k]["tolerance"])
+    out["seconds"] = time.perf_counter() - t0
+    return out
 
 
 def pcie_probe(hx, hy, dx, dy, n_bytes=1 << 30, reps=3):
@@ -238,20 +325,41 @@ def pcie_probe(hx, hy, dx, dy, n_bytes=1 << 30, reps=3):
     return out
 
 
-def ncu_traffic(C, T, mode, n_spectra_in):
+def ncu_traffic(C, T, mode, n_spectra_in, kernel_name):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
-    kernel, from the committed `ncu --set full` capture of this same
-    configuration (profiles/round1/traffic_*.json); None if there is none."""
+    kernel, from a committed `ncu --set full` capture of this same
+    configuration AND this same kernel (profiles/*/traffic_*.json, matched on
+    the kernel's template configuration); None if there is none."""
     import glob
-    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "traffic_*.json"))):
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "traffic_*.json")), reverse=True):
         try:
             t = json.load(open(f))
         except (OSError, ValueError):
             continue
+        cfg = kernel_name[kernel_name.find("<") + 1:] if "<" in kernel_name else kernel_name
         if (t.get("n_channels"), t.get("n_taps"), t.get("mode"), t.get("n_spectra_in")) == \
-                (C, T, mode, n_spectra_in):
-            return t["traffic_per_launch"]
-    return None
+                (C, T, mode, n_spectra_in) and cfg and cfg in t.get("kernel", ""):
+            return t["traffic_per_launch"], os.path.relpath(f, ROOT)
+    return None, None
+
+
+def time_steps(step, stream, steps):
+    """K timed steps on `stream`: (total seconds, mean per-launch seconds)."""
+    import torch
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    per = []
+    ev0.record(stream)
+    for _ in range(steps):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        step()
+        b.record(stream)
+        per.append((a, b))
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    return ev0.elapsed_time(ev1) / 1e3, float(np.mean([a.elapsed_time(b) for a, b in per])) / 1e3
 
 
 def main():
@@ -267,6 +375,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-mib", type=int, default=1024)
     ap.add_argument("--spectra", type=int, default=0, help="override S_in per GPU")
+    ap.add_argument("--no-exact", action="store_true", help="skip the EXACT-mode sub-record")
+    ap.add_argument("--no-parity", action="store_true", help="skip the whole-output check")
+    ap.add_argument("--parity-chunk-mib", type=int, default=512)
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -324,28 +435,14 @@ def main():
     sampler.start()
     time.sleep(0.3)
     launches0 = ppf.kernel_launches()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    per_launch = []
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    ev0.record(stream)
-    for _ in range(args.steps):
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        step()
-        b.record(stream)
-        per_launch.append((a, b))
-    ev1.record(stream)
-    torch.cuda.synchronize()
+    t_total, t_launch = time_steps(step, stream, args.steps)
     if world > 1:
         dist.barrier()
     launches = ppf.kernel_launches() - launches0
     clocks = sampler.stop()
-    t_total = ev0.elapsed_time(ev1) / 1e3
-    t_launch = float(np.mean([a.elapsed_time(b) for a, b in per_launch])) / 1e3
     t_max = max_over_ranks(t_total)
     in_all = sum_over_ranks(bytes_in)
     value = in_all * args.steps / t_max / 1e9
@@ -353,21 +450,44 @@ def main():
     peak, peak_src = measured_peak()
     achieved = alg_bytes / t_launch / 1e9
 
-    # ---- correctness spot check of the timed output (sampled rows vs oracle) ----
-    spot = None
-    if rank == 0:
-        import oracle
-        rows = [0, oc // 2, oc - 1]
-        errs = []
-        for r in rows:
-            lo = max(r - 2, 0)
-            hi = min(r + 3, oc)
-            xin = x[lo:hi + T - 1].cpu().numpy()
-            want = oracle.port().fir_fft(xin, C, T, coeffs.values).view(np.complex64)
-            got = y[lo:hi].cpu().numpy().reshape(-1)
-            d = np.abs(got.astype(np.complex128) - want.astype(np.complex128)).max()
-            errs.append(d / np.sqrt(np.mean(np.abs(want.astype(np.complex128)) ** 2)))
-        spot = float(max(errs))
+    # ---- the same step in the reference's precision (EXACT, bit-identical) ----
+    exact = None
+    y_exact = None
+    if args.mode == "fast" and not args.no_exact:
+        with ppf.Plan(C, T, coeffs, flags=ppf.EXACT, device=local_rank) as pe:
+            y_exact = torch.empty((oc, C), dtype=torch.complex64, device=dev)
+
+            def step_exact():
+                pe.fir_fft(x, out=y_exact)
+
+            for _ in range(args.warmup):
+                step_exact()
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            te_total, te_launch = time_steps(step_exact, stream, args.steps)
+            te_max = max_over_ranks(te_total)
+            v_exact = in_all * args.steps / te_max / 1e9
+            exact = {"value": v_exact, "unit": "GB/s", "x_realtime": v_exact * 1e9 / SKA_RATE,
+                     "ms_per_step": te_max / args.steps * 1e3,
+                     "dtype": "f64-acc FIR + f32 FFT (reference order)",
+                     "kernel": pe.kernel_name,
+                     "roofline": {"bound": "hbm", "achieved": alg_bytes / te_launch / 1e9,
+                                  "peak": peak, "unit": "GB/s",
+                                  "frac": alg_bytes / te_launch / 1e9 / peak,
+                                  "launch_ms": te_launch * 1e3}}
+
+    # ---- parity: every output spectrum of the timed runs vs the reference ----
+    parity = None
+    if rank == 0 and not args.no_parity:
+        outs = {args.mode: y}
+        if y_exact is not None:
+            outs["exact"] = y_exact
+        chunk = max(1, (args.parity_chunk_mib << 20) // (C * 8))
+        parity = full_parity(x, outs, C, T, coeffs.values, chunk)
+        if exact is not None:
+            exact["parity"] = parity.pop("exact")
+    del y_exact
 
     # ---- end to end through the public C-ABI with host buffers ----
     e2e = None
@@ -402,15 +522,25 @@ def main():
         workers = os.cpu_count() or 1
         sample = max(T, (args.cpu_sample_mib << 20) // (C * 8))
         gbs, kind, cores, secs = cpu_reference_sample(C, T, coeffs.values, sample, 2, workers)
+        sample1 = max(T, (args.cpu_sample_mib << 20) // 4 // (C * 8))
+        gbs1, _, cores1, secs1 = cpu_reference_sample(C, T, coeffs.values, sample1, 1, 1)
+        fir_gbs = cpu_fir_alone(C, T, coeffs.values, sample, 3, workers)
         cpu = {"value": gbs, "unit": "GB/s", "cores": cores, "kind": kind,
+               "cpu_model": cpu_model(), "host_threads": os.cpu_count(),
                "sample": f"{sample} spectra ({sample * C * 8 / 2**20:.0f} MiB) of the same "
                          f"workload, reference compute pass (bench.hpp:129-150), "
                          f"block_spectra=4096, median of {len(secs)}",
-               "x_realtime": gbs * 1e9 / SKA_RATE}
+               "x_realtime": gbs * 1e9 / SKA_RATE,
+               "single_core": {"value": gbs1, "unit": "GB/s", "cores": cores1,
+                               "sample": f"{sample1} spectra, same compute pass, workers=1"},
+               "fir_alone": {"value": fir_gbs, "unit": "GB/s", "cores": workers,
+                             "sample": f"{sample} spectra, ppf_fir_optimized one-shot "
+                                       f"(fir.hpp:158-212), best of 3"}}
 
     if rank == 0:
         kind = plan.kind
-        traffic = ncu_traffic(C, T, args.mode, ic)
+        kname = plan.kernel_name
+        traffic, traffic_src = ncu_traffic(C, T, args.mode, ic, kname)
         line = {
             "metric": METRIC,
             "value": value,
@@ -433,13 +563,17 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "bytes_per_launch": alg_bytes,
-                         "launch_ms": t_launch * 1e3},
+                         "launch_ms": t_launch * 1e3, "kernel": kname,
+                         "traffic_source": traffic_src},
+            "parity": parity.get(args.mode) if parity else None,
+            "exact": exact,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clocks,
             "gpu_launches": int(launches),
-            "spot_check_max_err_over_rms": spot,
         }
+        if parity:
+            line["parity"]["seconds"] = parity["seconds"]
         print(json.dumps(line), flush=True)
     plan.close()
     if world > 1:

@@ -24,6 +24,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <exception>
 #include <filesystem>
 #include <fstream>
 #include <functional>
@@ -482,21 +483,49 @@ inline StreamState process_stream(const PpfConfig& config, std::istream& source,
         coeffs = generate_prototype(config.n_channels, config.n_taps, config.window);
     }
     Plan p(config.n_channels, config.n_taps, coeffs.values.data());
+    // the callbacks run on library threads: an exception thrown by the
+    // istream / ostream (exceptions() enabled) is caught there, kept, and
+    // rethrown here once the library has returned
+    struct Io {
+        std::istream* is;
+        std::ostream* os;
+        std::exception_ptr read_exc, write_exc;
+    } io{&source, &sink, nullptr, nullptr};
     auto rd = [](void* ctx, void* buf, std::uint64_t n) -> std::int64_t {
-        auto& is = *static_cast<std::istream*>(ctx);
-        is.read(static_cast<char*>(buf), static_cast<std::streamsize>(n));
-        if (is.bad())
+        auto& c = *static_cast<Io*>(ctx);
+        try {
+            c.is->read(static_cast<char*>(buf), static_cast<std::streamsize>(n));
+            const std::streamsize got = c.is->gcount();
+            if (got > 0) // a partial read is processed first (pipeline.hpp:138-143)
+                return static_cast<std::int64_t>(got);
+            return c.is->bad() ? -1 : 0;
+        } catch (...) {
+            if (c.is->gcount() > 0) { // keep the delivered bytes; fail on the next read
+                c.read_exc = std::current_exception();
+                return static_cast<std::int64_t>(c.is->gcount());
+            }
+            c.read_exc = std::current_exception();
             return -1;
-        return static_cast<std::int64_t>(is.gcount());
+        }
     };
     auto wr = [](void* ctx, const void* buf, std::uint64_t n) -> int {
-        auto& os = *static_cast<std::ostream*>(ctx);
-        os.write(static_cast<const char*>(buf), static_cast<std::streamsize>(n));
-        return os ? 0 : 1;
+        auto& c = *static_cast<Io*>(ctx);
+        try {
+            c.os->write(static_cast<const char*>(buf), static_cast<std::streamsize>(n));
+            return *c.os ? 0 : 1;
+        } catch (...) {
+            c.write_exc = std::current_exception();
+            return 1;
+        }
     };
     ppfg_stream_state st{};
-    detail::check(ppfg_process_stream(p.get(), config.block_spectra, options.zero_prime ? 1 : 0,
-                                      config.fft_fallback ? 1 : 0, rd, &source, wr, &sink, &st));
+    const int rc = ppfg_process_stream(p.get(), config.block_spectra, options.zero_prime ? 1 : 0,
+                                       config.fft_fallback ? 1 : 0, rd, &io, wr, &io, &st);
+    if (rc == PPFG_IO_ERROR && io.write_exc)
+        std::rethrow_exception(io.write_exc);
+    if (rc == PPFG_DECODE_ERROR && io.read_exc)
+        std::rethrow_exception(io.read_exc);
+    detail::check(rc);
     sink.flush();
     if (!sink)
         throw io_error("process_stream: sink flush failed");

@@ -150,6 +150,10 @@ int ppfg_fir_fft_mean_power(ppfg_plan plan, const void* in, uint64_t n_spectra_i
  * 1 = fused FP32-FIR, 2 = fused FP64 (bit-exact) FIR, 3 / 4 = the cluster
  * versions of 1 / 2. */
 int ppfg_fir_fft_kind(ppfg_plan plan);
+/* The kernel ppfg_fir_fft launches for this plan, named the way ncu prints it
+ * ("fused_fir_fft_kernel<FusedCfg<10, 8, 2, 0, ...>>"), so measurements can be
+ * matched to profiles of exactly that kernel. Valid while the plan lives. */
+const char* ppfg_fir_fft_kernel_name(ppfg_plan plan);
 
 /* ---- single-row helpers (dft.hpp:39-66, 160-169), host memory ------------- */
 int ppfg_fft(const void* in, uint64_t n, void* out);        /* UNSUPPORTED_SIZE if n not 2^k */
@@ -177,9 +181,12 @@ int ppfg_stream_close(ppfg_stream stream, ppfg_stream_state* state);
 int ppfg_stream_destroy(ppfg_stream stream);
 
 /* process_stream (pipeline.hpp:89-200) over caller callbacks. read returns
- * the number of bytes produced (< n only at end of input, 0 = EOF, <0 =
- * source failure -> DECODE_ERROR); write returns 0 on success (non-zero ->
- * IO_ERROR, pipeline.hpp:131-132). */
+ * the number of bytes produced (any count <= n; it is called again until it
+ * returns 0 = end of input, or < 0 = source failure -> DECODE_ERROR at the
+ * offset after the bytes already delivered, pipeline.hpp:138-143); write
+ * returns 0 on success (non-zero -> IO_ERROR, pipeline.hpp:131-132). The
+ * callbacks run on library threads; they must not let C++ exceptions escape
+ * (one that does is treated as a failed read / write). */
 typedef int64_t (*ppfg_read_fn)(void* ctx, void* buf, uint64_t n);
 typedef int (*ppfg_write_fn)(void* ctx, const void* buf, uint64_t n);
 int ppfg_process_stream(ppfg_plan plan, uint64_t block_spectra, int zero_prime, int fft_fallback,
@@ -210,6 +217,10 @@ int ppfg_multi_fir_fft(uint64_t n_channels, uint64_t n_taps, const double* coeff
  * (seg_rows[g] + halo) - n_taps + 1 output spectra to d_out[g] — the stream's
  * outputs in order, byte-identical to one ppfg_fir_fft over the whole stream.
  * Plans share C and T; one host thread per segment; returns when all are done.
+ * Every segment's input must be complete when this is called: work queued on
+ * the plans' own streams is waited for, work on any other stream is the
+ * caller's to synchronise. An empty segment (seg_rows[g] == 0) may pass null
+ * buffers and gets out_rows[g] = 0.
  * Replaces the multi-worker one-shot of ppf_fir_optimized/channelize_block
  * (fir.hpp:158-212, dft.hpp:175-235) when the stream is sharded across GPUs. */
 int ppfg_multi_fir_fft_device(const ppfg_plan* plans, int n_segments, void* const* d_in,

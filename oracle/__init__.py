@@ -80,6 +80,7 @@ class _Port:
         L.ppfo_flops_for_fir.restype = C.c_uint64
         L.ppfo_flops_for_dft.argtypes = [_sz, _sz]
         L.ppfo_flops_for_dft.restype = C.c_uint64
+        L.ppfo_synth.argtypes = [_sz, C.c_uint64, C.c_uint64, _sz, _f32p]
 
     @staticmethod
     def _chk(st):
@@ -153,6 +154,12 @@ class _Port:
 
     def flops_for_fir(self, c, t, s):
         return self.lib.ppfo_flops_for_fir(c, t, s)
+
+    def synth(self, C_, n_samples, seed=1, first_sample=0):
+        """The bench's synthetic tone + noise (same bytes as ppfg_synth)."""
+        out = np.empty(2 * n_samples, np.float32)
+        self._chk(self.lib.ppfo_synth(C_, seed, first_sample, n_samples, out))
+        return out.view(np.complex64)
 
     def flops_for_dft(self, c, s):
         return self.lib.ppfo_flops_for_dft(c, s)

@@ -501,3 +501,44 @@ int ppfo_mean_power(const float* bins, size_t n_spectra, size_t n_channels, doub
             mean[c] /= (double)n_spectra;
     return PPFO_OK;
 }
+
+/* ---- synthetic workload (bench input; bytes identical to ppfg_synth) ---------- */
+static uint64_t synth_splitmix64(uint64_t z) {
+    z ^= z >> 30;
+    z *= 0xbf58476d1ce4e5b9ULL;
+    z ^= z >> 27;
+    z *= 0x94d049bb133111ebULL;
+    z ^= z >> 31;
+    return z;
+}
+
+static int synth_irwin_hall4(uint64_t z) {
+    return (int)((z & 0xffff) + ((z >> 16) & 0xffff) + ((z >> 32) & 0xffff) + (z >> 48)) - 131070;
+}
+
+int ppfo_synth(size_t n_channels, uint64_t seed, uint64_t first_sample, size_t n_samples,
+               float* out) {
+    if (n_channels == 0)
+        return PPFO_CONFIG_ERROR;
+    const uint64_t M = 10 * (uint64_t)n_channels, f10 = (10 * (uint64_t)n_channels) / 8 + 3;
+    float* tone = (float*)malloc(sizeof(float) * 2 * M);
+    if (!tone)
+        return PPFO_OTHER;
+    for (uint64_t k = 0; k < M; ++k) {
+        const double a = 2.0 * M_PI * (double)k / (double)M;
+        tone[2 * k] = (float)cos(a);
+        tone[2 * k + 1] = (float)sin(a);
+    }
+    const uint64_t golden = 0x9e3779b97f4a7c15ULL;
+    const float scale = 2.64293e-05f;
+    for (size_t i = 0; i < n_samples; ++i) {
+        const uint64_t n = first_sample + i;
+        const uint64_t t = (f10 * n) % M;
+        const float gr = (float)synth_irwin_hall4(synth_splitmix64(seed + (2 * n + 1) * golden)) * scale;
+        const float gi = (float)synth_irwin_hall4(synth_splitmix64(seed + (2 * n + 2) * golden)) * scale;
+        out[2 * i] = tone[2 * t] + gr;
+        out[2 * i + 1] = tone[2 * t + 1] + gi;
+    }
+    free(tone);
+    return PPFO_OK;
+}

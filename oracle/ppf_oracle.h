@@ -39,7 +39,8 @@ enum {
     PPFO_DEGENERATE_FILTER = 4,
     PPFO_DECODE_ERROR = 5,
     PPFO_IO_ERROR = 6,
-    PPFO_DOMAIN_ERROR = 9
+    PPFO_DOMAIN_ERROR = 9,
+    PPFO_OTHER = 99
 };
 
 /* coeff.hpp:61-65 */
@@ -94,6 +95,15 @@ typedef struct {
 int ppfo_process_stream(size_t n_channels, size_t n_taps, size_t block_spectra, int fft_fallback,
                         int zero_prime, const double* coeff_values, const uint8_t* src,
                         size_t src_len, uint8_t* out, ppfo_stream_state* state);
+
+/* The bench's synthetic workload (not a reference function):
+ * x[n] = tone[(f10*n) mod 10C] + (g_re + i g_im), tone = f32 e^{2 pi i k/(10C)},
+ * f10 = 10C/8 + 3, g = Irwin-Hall(4 x 16 bit of splitmix64(seed + (2n+1|2n+2)
+ * * golden))) * 2.64293e-05f. Integer + IEEE-rounded float ops only, so the
+ * bytes equal the product's device generator (libppfg ppfg_synth); used to
+ * feed the reference's CPU arm without loading the product library. */
+int ppfo_synth(size_t n_channels, uint64_t seed, uint64_t first_sample, size_t n_samples,
+               float* out);
 
 #ifdef __cplusplus
 }

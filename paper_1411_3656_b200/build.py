@@ -17,8 +17,8 @@ NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
     "-Xcompiler", "-fPIC,-ffp-contract=off",
-    "-shared",
 ]
+OBJ_DIR = os.path.join(PKG, "_obj")
 
 
 def _nvcc():
@@ -28,9 +28,19 @@ def _nvcc():
     return "nvcc"
 
 
-def sources():
-    return sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cuh"))
+def units():
+    """The translation units: ppfg.cu (host code + small kernels) and the
+    tab_*.cu kernel-table units, compiled in parallel."""
+    return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+
+
+def headers():
+    return sorted(glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h"))
                   + glob.glob(os.path.join(INCLUDE, "*.h")))
+
+
+def sources():
+    return units() + headers()
 
 
 def stale() -> bool:
@@ -40,11 +50,35 @@ def stale() -> bool:
     return any(os.path.getmtime(s) > t for s in sources())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def _obj(cu):
+    return os.path.join(OBJ_DIR, os.path.basename(cu)[:-3] + ".o")
+
+
+def build(force: bool = False, verbose: bool = False, jobs: int = 0) -> str:
     if not force and not stale():
         return SO
+    from concurrent.futures import ThreadPoolExecutor
+    os.makedirs(OBJ_DIR, exist_ok=True)
+    newest_header = max(os.path.getmtime(h) for h in headers())
+
+    def compile_one(cu):
+        obj = _obj(cu)
+        if not force and os.path.exists(obj) and os.path.getmtime(obj) >= max(
+                os.path.getmtime(cu), newest_header):
+            return obj
+        tmp = obj + f".tmp{os.getpid()}"
+        cmd = [_nvcc(), *NVCC_FLAGS, "-I" + INCLUDE, "-c", "-o", tmp, cu]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.check_call(cmd)
+        os.replace(tmp, obj)
+        return obj
+
+    jobs = jobs or min(len(units()), os.cpu_count() or 1)
+    with ThreadPoolExecutor(max_workers=jobs) as ex:
+        objs = list(ex.map(compile_one, units()))
     tmp = SO + f".tmp{os.getpid()}"
-    cmd = [_nvcc(), *NVCC_FLAGS, "-I" + INCLUDE, "-o", tmp, os.path.join(CSRC, "ppfg.cu")]
+    cmd = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)

@@ -11,7 +11,7 @@ namespace ppfg {
 // into acc += fma(xr, wr, -(xi*wi)) / acc += fma(xr, wi, xi*wr) when built the
 // way proj/CMakeLists.txt builds it (pinned in tests/test_oracle.py); the same
 // operations are written out here with _rn intrinsics.
-__global__ void __launch_bounds__(256) dft_naive_kernel(const float2* __restrict__ in,
+static __global__ void __launch_bounds__(256) dft_naive_kernel(const float2* __restrict__ in,
                                                         float2* __restrict__ out, unsigned n,
                                                         long long n_rows,
                                                         const double2* __restrict__ roots) {
@@ -60,7 +60,7 @@ PPFG_HD int irwin_hall4(uint64_t z) {
 constexpr uint64_t kGolden = 0x9e3779b97f4a7c15ULL;
 constexpr float kNoiseScale = 2.64293e-05f; // 1 / sqrt(4 * (65536^2 - 1) / 12)
 
-__global__ void __launch_bounds__(256) synth_kernel(float2* __restrict__ out, uint64_t seed,
+static __global__ void __launch_bounds__(256) synth_kernel(float2* __restrict__ out, uint64_t seed,
                                                     uint64_t first, uint64_t count, uint64_t f10,
                                                     uint64_t M, const float2* __restrict__ tone) {
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;

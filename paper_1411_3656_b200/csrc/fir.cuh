@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(256, 3) fir_fast_kernel(const __grid_constant_
 }
 
 // Any T: the same op sequence, window re-read through L1/L2 per tap.
-__global__ void __launch_bounds__(256) fir_exact_generic_kernel(const float2* __restrict__ in,
+static __global__ void __launch_bounds__(256) fir_exact_generic_kernel(const float2* __restrict__ in,
                                                                 float2* __restrict__ out,
                                                                 unsigned C, unsigned T,
                                                                 long long S_out,

@@ -358,7 +358,7 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
 
 // Per-channel mean power from per-CTA partials: mean[c] = (sum over parts,
 // in a fixed order) / n — deterministic for a given grid.
-__global__ void power_reduce_kernel(const double* __restrict__ part, int n_parts, int C,
+static __global__ void power_reduce_kernel(const double* __restrict__ part, int n_parts, int C,
                                     double n, double* __restrict__ mean) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= C)
@@ -372,7 +372,7 @@ __global__ void power_reduce_kernel(const double* __restrict__ part, int n_parts
 // cmd_inspect on channelized bins (cli.hpp:307-317): CTA g sums the powers of
 // spectra [g*rows_per_cta, ...) per channel (thread = channel stripe), in
 // spectrum order, into part[g][c].
-__global__ void __launch_bounds__(256) power_partial_kernel(const float2* __restrict__ bins,
+static __global__ void __launch_bounds__(256) power_partial_kernel(const float2* __restrict__ bins,
                                                             long long n_spectra, int C,
                                                             long long rows_per_cta,
                                                             double* __restrict__ part) {

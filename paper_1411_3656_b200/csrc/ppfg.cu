@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "ppfg.h"
+#include "tables.h"
 
 #include "dft.cuh"
 #include "fft.cuh"
@@ -88,289 +89,17 @@ struct DeviceGuard {
 };
 
 // -------------------------------------------------------- kernel tables
-using KernelFn = const void*;
-
-struct FusedEntry {
-    int L, T;
-    bool exact;
-    KernelFn fn;
-    size_t smem;
-    int nt;
-    int rows_per_batch; // B * G
-    int q;              // CTAs per cluster (1: single-SM kernel)
-    bool preferred;     // cluster kernels: faster than FIR -> HBM -> FFT (measured)
-    int map_r = 0;      // > 0: the kernel reads its input through a 3-D TMA tensor
-    int map_rb = 0;     //      map with box {map_run, map_r, map_rb} (fused_split.cuh)
-    int map_run = 0;
-    KernelFn power_fn = nullptr; // detection variant (POWER), single-SM entries
-    int power_rows = 0;          // its partials per CTA (tile rows)
-    bool tw4 = false;            // takes the pre-expanded float4 twiddle table
-};
-
-// The detection variant exists where every FFT thread's last-pass units see
-// the same bins (FusedCfg::POWER_OK), so its accumulators stay per bin.
-template <class Cfg>
-constexpr bool has_power() {
-    return Cfg::POWER_OK;
-}
-
-template <class Cfg>
-FusedEntry fused_entry() {
-    FusedEntry e{Cfg::L,    Cfg::T,  Cfg::EXACT, reinterpret_cast<KernelFn>(&fused_fir_fft_kernel<Cfg>),
-                 Cfg::SMEM, Cfg::NT, Cfg::B * Cfg::G, 1, true};
-    e.tw4 = Cfg::TW4;
-    if constexpr (has_power<Cfg>()) {
-        e.power_fn = reinterpret_cast<KernelFn>(&fused_fir_fft_kernel<Cfg, true>);
-        e.power_rows = Cfg::POWER_ROWS;
-    }
-    return e;
-}
-
-template <class Cfg>
-FusedEntry split_entry(bool preferred) {
-    FusedEntry e{Cfg::L,    Cfg::T,  Cfg::EXACT, reinterpret_cast<KernelFn>(&fused_split_kernel<Cfg>),
-                 Cfg::SMEM, Cfg::NT, Cfg::B,     Cfg::Q,
-                 preferred, Cfg::R,  Cfg::RB,    Cfg::RUN};
-    e.tw4 = Cfg::TW4;
-    if constexpr (Cfg::POWER_OK) {
-        e.power_fn = reinterpret_cast<KernelFn>(&fused_split_kernel<Cfg, true>);
-        e.power_rows = Cfg::POWER_ROWS;
-    }
-    return e;
-}
-
-// Which (C, T) get a fused kernel. Register budget per SM ~ C * (3T fp32 |
-// 6T fp64) for the FIR windows + taps, plus the FFT pass registers. Entries
-// with (120, 80, 2, 3) run three FFT warpgroups (640 threads): measured faster
-// where the FFT role is critical (C=1024/T=8, C=64, T=1 at C<=128), slower
-// elsewhere (round-1 sweep, profiles/round1/sweep.md).
+// (tables.h; the kernel instantiations are compiled in the tab_*.cu units)
 const std::vector<FusedEntry>& fused_table() {
-    static const std::vector<FusedEntry> t = {
-        // (float4 twiddle tables where they measured faster than float2:
-        // C=1024 T=8 FAST 0.86 vs 0.85 at the SKA size, C=512 EXACT 0.68 vs
-        // 0.65, C=64 0.88 vs 0.86, EXACT C=64..256 +2-3 %; L2 prefetch one
-        // chunk ahead at the SKA shape: 2836 vs 2802 GB/s on the 6.5 GB
-        // bench (flat at 1 GiB; -1..2 % on other shapes); three FFT
-        // warpgroups at C=128 0.87 vs 0.78, C=256 0.82 vs 0.76, C=512 0.91 vs
-        // 0.90 — but not at C=1024 T=4: 0.83 vs 0.86; FIR/FFT registers
-        // 136/120 instead of 160/96 at C=512 T=16 0.76 vs 0.72 and FP64
-        // C=1024 T=4 0.762 vs 0.753)
-        fused_entry<FusedCfg<10, 8, 2, false, 120, 80, 2, 3, 2, true, 1>>(),
-        fused_entry<FusedCfg<9, 8, 2, false, 120, 80, 2, 3>>(),
-        fused_entry<FusedCfg<8, 8, 2, false, 120, 80, 2, 3>>(),
-        fused_entry<FusedCfg<7, 8, 2, false, 120, 80, 2, 3>>(),
-        fused_entry<FusedCfg<6, 8, 1, false, 120, 80, 2, 3, 2, true>>(),
-        fused_entry<FusedCfg<10, 4, 2, false>>(),
-        fused_entry<FusedCfg<9, 16, 1, false, 136, 120>>(),
-        fused_entry<FusedCfg<9, 8, 1, true, 160, 96, 4, 2, 2, true>>(),
-        fused_entry<FusedCfg<8, 8, 1, true, 160, 96, 4, 2, 2, true>>(),
-        fused_entry<FusedCfg<7, 8, 1, true, 160, 96, 4, 2, 2, true>>(),
-        fused_entry<FusedCfg<6, 8, 1, true, 160, 96, 4, 2, 2, true>>(),
-        fused_entry<FusedCfg<10, 4, 2, true, 136, 120>>(),
-        // small C at T = 4 and 16 (register budget: 3T·R FP32, 6T·R FP64 per FIR thread)
-        fused_entry<FusedCfg<8, 16, 1, false>>(),
-        fused_entry<FusedCfg<7, 16, 1, false>>(),
-        fused_entry<FusedCfg<6, 16, 1, false>>(),
-        fused_entry<FusedCfg<8, 16, 0, true>>(),
-        fused_entry<FusedCfg<7, 16, 0, true>>(),
-        fused_entry<FusedCfg<6, 16, 0, true>>(),
-        fused_entry<FusedCfg<9, 4, 2, false>>(),
-        fused_entry<FusedCfg<8, 4, 2, false>>(),
-        fused_entry<FusedCfg<7, 4, 2, false>>(),
-        fused_entry<FusedCfg<6, 4, 1, false>>(),
-        fused_entry<FusedCfg<9, 4, 2, true>>(),
-        fused_entry<FusedCfg<8, 4, 2, true>>(),
-        fused_entry<FusedCfg<7, 4, 2, true>>(),
-        fused_entry<FusedCfg<6, 4, 1, true>>(),
-        fused_entry<FusedCfg<8, 32, 0, false>>(),
-        fused_entry<FusedCfg<7, 32, 0, false>>(),
-        fused_entry<FusedCfg<6, 32, 0, false>>(),
-        // T = 1 with unit taps: x*1 == x exactly, so these are bit-exact,
-        // TMA-fed, warp-specialised FFTs — channelize_block for 64 <= C <= 4096
-        // (C = 4096: 0.76 of roofline vs 0.69 for K2)
-        // (split-kernel T = 1 entries for C = 4096, 8192 and FP64 C = 4096 on
-        // 8-CTA clusters measured slower than K2 / the unfused path)
-        fused_entry<FusedCfg<6, 1, 0, false, 120, 80, 2, 3>>(),
-        fused_entry<FusedCfg<7, 1, 0, false, 120, 80, 2, 3>>(),
-        fused_entry<FusedCfg<8, 1, 0, false>>(),
-        fused_entry<FusedCfg<9, 1, 1, false>>(),
-        fused_entry<FusedCfg<10, 1, 2, false>>(),
-        fused_entry<FusedCfg<11, 1, 3, false, 160, 96, 3>>(),
-        fused_entry<FusedCfg<12, 1, 4, false, 160, 96, 2>>(),
-        // thread-block clusters, FIR split by channel block and FFT by
-        // spectrum (fused_split.cuh) — for FIR state that does not fit one SM.
-        // preferred = taken by default: measured faster than FIR -> HBM -> FFT
-        // (round 1, 1 GiB inputs: C=1024 T=16 0.62 vs 0.32 of HBM roofline,
-        // T=32 0.41 vs 0.18, FP64 T=8 0.62 vs 0.42, FP64 T=16 0.40 vs 0.32,
-        // C=2048 0.51 vs 0.42, FP64 C=2048 0.47 vs 0.42, C=4096 0.43 vs 0.38;
-        // C=8192 0.29 vs 0.32 stays opt-in via PPFG_CLUSTER)
-        // (float4 twiddle tables where they measured faster: FAST C=1024
-        // T=16 0.62 vs 0.58, EXACT C=1024 T=16 0.40 vs 0.39, EXACT C=2048
-        // 0.47 vs 0.44; FAST C=2048/4096 gained 15-27 % from float2)
-        // (T=32 FAST: the unfused K1b FP32 FIR -> FFT measured 0.43 vs 0.42;
-        // FIR/FFT registers 136/120 instead of 152/104 at FAST C=1024 T=16
-        // 0.645 vs 0.619 and C=2048 0.688 vs 0.624 — not at C=4096 or FP64 C=2048;
-        // FP64 C=1024 T=8 with float4 twiddles 0.629 vs 0.620 over four A/B
-        // pairs; 4-CTA clusters 0.51, W=4 passes 0.44, FIR 168/88 0.44.
-        // Rejected in the same A/B: FAST C=4096 float4 0.42 / 8-CTA 0.31 vs
-        // 0.53; FP64 T=16 168/88 0.402 vs 0.403; FAST T=32 cluster 136/120
-        // 0.41, 168/88 0.42, 8-CTA 0.28 — all below unfused K1b 0.43)
-
-        split_entry<SplitCfg<10, 1, 16, false, 2, 5, 136, 120, 0, true>>(true),
-        split_entry<SplitCfg<10, 2, 32, false, 2, 5, 152, 104, 0, true>>(false),
-        split_entry<SplitCfg<10, 1, 8, true, 2, 5, 136, 120, 0, true>>(true),
-        split_entry<SplitCfg<10, 2, 16, true, 2, 5, 152, 104, 0, true>>(true),
-        split_entry<SplitCfg<11, 1, 8, false, 2, 5, 136, 120>>(true),
-        split_entry<SplitCfg<11, 2, 8, true, 2, 5, 152, 104, 0, true>>(true),
-        split_entry<SplitCfg<12, 2, 8, false>>(true),
-        split_entry<SplitCfg<13, 3, 8, false>>(false),
-
-    };
-    return t;
-}
-
-struct FftEntry {
-    KernelFn fn;
-    size_t smem;
-    int nt;
-    int rows_per_tile;
-};
-
-constexpr int kFftW = 5;
-constexpr int kFftNT = 256;
-constexpr int kFftMaxL = 13;
-constexpr int kRingNT = 0; // K2r threads per CTA (0: one first-pass unit per thread; 512 measured the same)
-
-template <int L>
-FftEntry fft_entry() {
-    constexpr bool tws = L <= 11;
-    constexpr int rb = (kFftNT << kFftW) / (1 << L) > 0 ? (kFftNT << kFftW) / (1 << L) : 1;
-    return {reinterpret_cast<KernelFn>(&fft_rows_kernel<L, kFftW, tws, kFftNT>),
-            fft_rows_smem_bytes<L, kFftW, tws, kFftNT>(), kFftNT, rb};
-}
-
-const FftEntry* fft_table(int L) {
-    static const FftEntry t[kFftMaxL + 1] = {
-        {nullptr, 0, 0, 0},  fft_entry<1>(),  fft_entry<2>(),  fft_entry<3>(),  fft_entry<4>(),
-        fft_entry<5>(),      fft_entry<6>(),  fft_entry<7>(),  fft_entry<8>(),  fft_entry<9>(),
-        fft_entry<10>(),     fft_entry<11>(), fft_entry<12>(), fft_entry<13>(),
-    };
-    if (L < 1 || L > kFftMaxL)
-        return nullptr;
-    return &t[L];
-}
-
-struct FirEntry {
-    KernelFn fn;
-    int tc, k; // taps per lane, lanes per channel (T = tc * k)
-};
-
-template <int TC, int K>
-FirEntry fir_entry() {
-    constexpr int LAG = K == 1 ? 1 : (TC % 4 == 0 ? 4 : (TC % 2 == 0 ? 2 : 1));
-    return {reinterpret_cast<KernelFn>(&fir_chain_kernel<TC, K, LAG>), TC, K};
-}
-
-// K1 variants: one lane per channel up to T = 16; larger T split over K
-// lanes of up to 16 taps (T = TC * K), chained with a lag (fir.cuh).
-struct FirTmaEntry {
-    KernelFn fn = nullptr;
-    int k = 0, rb = 0;
-    size_t smem = 0;
-};
-
-template <int TC, int K, int RB, int MINB = 2>
-FirTmaEntry fir_tma_entry() {
-    constexpr int LAG = K == 1 ? 1 : (TC % 4 == 0 ? 4 : (TC % 2 == 0 ? 2 : 1));
-    using F = FirTma<TC, K, LAG, RB>;
-    return {reinterpret_cast<KernelFn>(&fir_tma_kernel<TC, K, LAG, RB, MINB>), K, RB, F::SMEM};
-}
-
-// K1t shapes (TMA-staged input; measured FIR-only at C = 1024: T = 8 0.87 vs
-// 0.79, T = 16 0.66 vs 0.50, T = 32 (one lane per channel, 244 registers,
-// 8 warps/SM) 0.36 vs 0.23 of the HBM roofline). Lane-chained K1t variants
-// measured slower than the register-prefetch K1, which keeps the other T.
-FirTmaEntry fir_tma_table(int T) {
-    switch (T) {
-    case 4: return fir_tma_entry<4, 1, 8>();
-    case 8: return fir_tma_entry<8, 1, 8>();
-    case 12: return fir_tma_entry<12, 1, 8>();
-    case 16: return fir_tma_entry<16, 1, 8>();
-    case 32: return fir_tma_entry<32, 1, 8, 1>();
-    default: return {};
-    }
-}
-
-template <int TC, int K, int RB>
-FirTmaEntry fir_fast_entry() {
-    return {reinterpret_cast<KernelFn>(&fir_fast_kernel<TC, K, RB>), K, RB, FirFast<TC, K, RB>::SMEM};
-}
-
-// K1f shapes: FP32 FIR for PPFG_FAST where no fused kernel covers T
-FirTmaEntry fir_fast_table(int T) {
-    switch (T) {
-    case 32: return fir_fast_entry<16, 2, 8>();
-    case 64: return fir_fast_entry<16, 4, 8>();
-    case 128: return fir_fast_entry<16, 8, 8>();
-    default: return {};
-    }
-}
-
-// K1b shapes (register-blocked, CTA-wide TMA ring; fir.cuh): U = 16 outputs
-// per thread, 4 warps per CTA
-struct FirBlkEntry {
-    KernelFn fn = nullptr;
-    int rb = 0, nt = 0;
-    size_t smem = 0;
-};
-
-template <int T, int U, int NW, bool EXACT, int MINB>
-FirBlkEntry fir_blk_entry() {
-    using F = FirBlk<T, U, NW, EXACT>;
-    return {reinterpret_cast<KernelFn>(&fir_block_kernel<T, U, NW, EXACT, MINB>), F::RB, F::NT,
-            F::SMEM};
-}
-
-FirBlkEntry fir_blk_table(int T, bool exact) {
-    if (exact) {
-        switch (T) {
-        case 16: return fir_blk_entry<16, 16, 4, true, 3>();
-        case 20: return fir_blk_entry<20, 16, 4, true, 3>();
-        case 24: return fir_blk_entry<24, 16, 4, true, 3>();
-        case 32: return fir_blk_entry<32, 16, 4, true, 3>();
-        case 48: return fir_blk_entry<48, 16, 4, true, 2>();
-        case 64: return fir_blk_entry<64, 16, 4, true, 2>();
-        default: return {};
+    static const std::vector<FusedEntry> t = [] {
+        std::vector<FusedEntry> v;
+        for (auto part : {fused_part_main, fused_part_small, fused_part_fft, fused_part_split}) {
+            auto p = part();
+            v.insert(v.end(), p.begin(), p.end());
         }
-    }
-    switch (T) {
-    case 16: return fir_blk_entry<16, 16, 4, false, 3>();
-    case 24: return fir_blk_entry<24, 16, 4, false, 3>();
-    case 32: return fir_blk_entry<32, 16, 4, false, 3>();
-    case 48: return fir_blk_entry<48, 16, 4, false, 3>();
-    case 64: return fir_blk_entry<64, 16, 4, false, 3>();
-    case 96: return fir_blk_entry<96, 16, 4, false, 2>();
-    case 128: return fir_blk_entry<128, 16, 2, false, 3>();
-    default: return {};
-    }
-}
-
-FirEntry fir_table(int T) {
-    switch (T) {
-#define PPFG_FIR(t, tc, k)                                                                        \
-    case t:                                                                                       \
-        return fir_entry<tc, k>();
-        PPFG_FIR(1, 1, 1) PPFG_FIR(2, 2, 1) PPFG_FIR(3, 3, 1) PPFG_FIR(4, 4, 1)
-        PPFG_FIR(5, 5, 1) PPFG_FIR(6, 6, 1) PPFG_FIR(7, 7, 1) PPFG_FIR(8, 8, 1)
-        PPFG_FIR(9, 9, 1) PPFG_FIR(10, 10, 1) PPFG_FIR(11, 11, 1) PPFG_FIR(12, 12, 1)
-        PPFG_FIR(13, 13, 1) PPFG_FIR(14, 14, 1) PPFG_FIR(15, 15, 1) PPFG_FIR(16, 16, 1)
-        PPFG_FIR(20, 10, 2) PPFG_FIR(24, 12, 2) PPFG_FIR(28, 14, 2) PPFG_FIR(32, 16, 2)
-        PPFG_FIR(40, 10, 4) PPFG_FIR(48, 16, 3) PPFG_FIR(56, 14, 4) PPFG_FIR(64, 16, 4)
-        PPFG_FIR(96, 16, 6) PPFG_FIR(128, 16, 8)
-#undef PPFG_FIR
-    default:
-        return {nullptr, 0, 0};
-    }
+        return v;
+    }();
+    return t;
 }
 
 // one-time per (device, function) opt-in to large dynamic shared memory
@@ -396,7 +125,9 @@ int ensure_smem_attr(KernelFn fn, size_t smem, int device) {
 // drop-in creates a plan per process_stream call).
 struct PsBuffers {
     static constexpr int KH = 3, KD = 2, KO = 3;
-    uint64_t io = 0, rows_cap = 0, taps = 0;
+    // byte capacity of each buffer set: the reuse check compares bytes, never
+    // row counts (a pooled set may have been sized for another row size)
+    uint64_t hin_cap = 0, din_cap = 0, out_cap = 0;
     void* h_in[KH] = {};
     void* h_out[KO] = {};
     void* d_in[KD] = {};
@@ -427,24 +158,28 @@ struct PsBuffers {
         for (auto& e : ev_d2h)
             if (e)
                 cudaEventDestroy(e), e = nullptr;
-        io = rows_cap = taps = 0;
+        hin_cap = din_cap = out_cap = 0;
     }
-    // (re)allocate for blocks of io bytes (+ one spectrum of carry) and T taps
+    // (re)allocate for blocks of io bytes (+ one spectrum of carry) of
+    // row_bytes-byte spectra behind T-1 history rows
     bool ensure(uint64_t io_, uint64_t row_bytes, uint64_t T) {
         const uint64_t rows = io_ / row_bytes + 1;
-        if (io >= io_ && rows_cap >= rows && taps == T)
+        const uint64_t need_hin = io_ + row_bytes;
+        const uint64_t need_din = (T - 1 + rows) * row_bytes;
+        const uint64_t need_out = rows * row_bytes;
+        if (hin_cap >= need_hin && din_cap >= need_din && out_cap >= need_out)
             return true;
         release();
         bool ok = true;
         for (int i = 0; i < KH && ok; ++i)
-            ok = cudaMallocHost(&h_in[i], io_ + row_bytes) == cudaSuccess &&
+            ok = cudaMallocHost(&h_in[i], need_hin) == cudaSuccess &&
                  cudaEventCreateWithFlags(&ev_hin[i], cudaEventDisableTiming) == cudaSuccess;
         for (int i = 0; i < KO && ok; ++i)
-            ok = cudaMallocHost(&h_out[i], rows * row_bytes) == cudaSuccess &&
-                 cudaMalloc(&d_out[i], rows * row_bytes) == cudaSuccess &&
+            ok = cudaMallocHost(&h_out[i], need_out) == cudaSuccess &&
+                 cudaMalloc(&d_out[i], need_out) == cudaSuccess &&
                  cudaEventCreateWithFlags(&ev_d2h[i], cudaEventDisableTiming) == cudaSuccess;
         for (int i = 0; i < KD && ok; ++i)
-            ok = cudaMalloc(&d_in[i], (T - 1 + rows) * row_bytes) == cudaSuccess &&
+            ok = cudaMalloc(&d_in[i], need_din) == cudaSuccess &&
                  cudaEventCreateWithFlags(&ev_din[i], cudaEventDisableTiming) == cudaSuccess &&
                  cudaEventCreateWithFlags(&ev_comp[i], cudaEventDisableTiming) == cudaSuccess;
         if (!ok) {
@@ -452,9 +187,9 @@ struct PsBuffers {
             cudaGetLastError();
             return false;
         }
-        io = io_;
-        rows_cap = rows;
-        taps = T;
+        hin_cap = need_hin;
+        din_cap = need_din;
+        out_cap = need_out;
         return true;
     }
 };
@@ -475,6 +210,7 @@ struct ppfg_plan_s {
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     const FusedEntry* fused = nullptr;
+    std::string fused_name; // the fused kernel's configuration, as ncu prints it
     // host-mode pipeline buffers (grow-only)
     void* d_in[2] = {nullptr, nullptr};
     void* d_out[2] = {nullptr, nullptr};
@@ -835,16 +571,15 @@ int launch_channelize(ppfg_plan p, const float2* din, uint64_t rows, float2* dou
     // C = 8192: the TMA-ring row FFT (0.73 of the HBM roofline vs 0.57 for
     // K2; at C = 4096 it measured 0.82 vs 0.83 for the T = 1 fused kernel)
     if (L == 13 && reinterpret_cast<uintptr_t>(din) % 16 == 0) {
-        using F = FftRing<13, kFftW, kRingNT>;
-        KernelFn fn = reinterpret_cast<KernelFn>(&fft_ring_kernel<13, kFftW, kRingNT>);
-        PPFG_TRY(ensure_smem_attr(fn, F::SMEM, p->device));
+        const FftEntry fr = fft_ring_entry();
+        PPFG_TRY(ensure_smem_attr(fr.fn, fr.smem, p->device));
         int per_sm = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, F::NT, F::SMEM);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fr.fn, fr.nt, fr.smem);
         const uint64_t grid =
             std::min<uint64_t>(rows, static_cast<uint64_t>(p->num_sms) * std::max(per_sm, 1));
         long long rows_ll = static_cast<long long>(rows);
         void* args[] = {&din, &dout, &rows_ll, &p->d_tw};
-        PPFG_CUDA(cudaLaunchKernel(fn, dim3(static_cast<unsigned>(grid)), dim3(F::NT), args, F::SMEM, st));
+        PPFG_CUDA(cudaLaunchKernel(fr.fn, dim3(static_cast<unsigned>(grid)), dim3(fr.nt), args, fr.smem, st));
         return check_launch("fft kernel (TMA ring)");
     }
     // T = 1 fused kernel with unit taps (in place is safe: row s is written
@@ -1236,6 +971,24 @@ std::vector<float2> host_tone(uint64_t C) {
 
 uint64_t tone_f10(uint64_t C) { return (10 * C) / 8 + 3; }
 
+// "fused_fir_fft_kernel<FusedCfg<10, 8, 2, 0, ...>>" from the entry maker's
+// __PRETTY_FUNCTION__ ("... [with Cfg = ppfg::FusedCfg<10, 8, 2, false, ...>]"),
+// spelled the way ncu prints the template arguments (bools as 0/1)
+std::string kernel_name_of(const FusedEntry& e) {
+    std::string sig = e.sig ? e.sig : "";
+    const size_t at = sig.find("Cfg = ");
+    std::string cfg = at == std::string::npos ? sig : sig.substr(at + 6);
+    if (!cfg.empty() && cfg.back() == ']')
+        cfg.pop_back();
+    for (const char* ns : {"ppfg::"})
+        for (size_t k; (k = cfg.find(ns)) != std::string::npos;)
+            cfg.erase(k, std::strlen(ns));
+    for (auto [from, to] : {std::pair<const char*, const char*>{"false", "0"}, {"true", "1"}})
+        for (size_t k; (k = cfg.find(from)) != std::string::npos;)
+            cfg.replace(k, std::strlen(from), to);
+    return std::string(e.q > 1 ? "fused_split_kernel<" : "fused_fir_fft_kernel<") + cfg + ">";
+}
+
 } // namespace
 
 // ================================================================ C-ABI
@@ -1354,6 +1107,7 @@ int ppfg_plan_create(ppfg_plan* plan, uint64_t n_channels, uint64_t n_taps,
             if (e.L == p->L && e.T == static_cast<int>(n_taps) && e.exact == exact &&
                 (e.q == 1 || want_cluster || e.preferred)) {
                 p->fused = &e;
+                p->fused_name = kernel_name_of(e);
                 break;
             }
         }
@@ -1400,6 +1154,14 @@ int ppfg_plan_destroy(ppfg_plan p) {
 }
 
 void* ppfg_plan_stream(ppfg_plan plan) { return plan ? plan->stream : nullptr; }
+
+const char* ppfg_fir_fft_kernel_name(ppfg_plan p) {
+    if (!p)
+        return "";
+    if (!p->fused || (p->flags & PPFG_UNFUSED))
+        return "unfused (FIR kernel + FFT kernel)";
+    return p->fused_name.c_str();
+}
 
 int ppfg_fir_fft_kind(ppfg_plan p) {
     if (!p || !p->fused || (p->flags & PPFG_UNFUSED))
@@ -1587,6 +1349,9 @@ int ppfg_multi_fir_fft_device(const ppfg_plan* plans, int n_segments, void* cons
             ppfg_plan p = plans[g];
             DeviceGuard dg(p->device);
             auto body = [&]() -> int {
+                out_rows[g] = 0;
+                if (seg_rows[g] == 0) // an empty segment has no outputs (and may have no buffer)
+                    return PPFG_OK;
                 // halo: the next T-1 rows of the stream, from the following segment(s)
                 uint64_t have = seg_rows[g];
                 uint64_t need = T - 1;
@@ -1602,6 +1367,19 @@ int ppfg_multi_fir_fft_device(const ppfg_plan* plans, int n_segments, void* cons
                         else if (e != cudaSuccess)
                             return fail(PPFG_CUDA_ERROR, std::string("peer access: ") + cudaGetErrorString(e));
                     }
+                    // the peer segment must be complete: order the copy after
+                    // the work queued on its plan's stream (work on other streams
+                    // is the caller's to finish, see ppfg.h)
+                    cudaEvent_t ready = nullptr;
+                    {
+                        DeviceGuard pk(dk);
+                        PPFG_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+                        PPFG_CUDA(cudaEventRecord(ready, plans[k]->stream));
+                    }
+                    const cudaError_t we = cudaStreamWaitEvent(p->stream, ready, 0);
+                    cudaEventDestroy(ready);
+                    if (we != cudaSuccess)
+                        return fail(PPFG_CUDA_ERROR, std::string("peer halo wait: ") + cudaGetErrorString(we));
                     PPFG_CUDA(cudaMemcpyPeerAsync(static_cast<char*>(d_in[g]) + have * row_bytes, p->device,
                                                   d_in[k], dk, take * row_bytes, p->stream));
                     have += take;
@@ -1837,7 +1615,14 @@ int process_stream_pipelined(ppfg_plan p, uint64_t block_spectra, int zero_prime
             char* slot = static_cast<char*>(h_in[h]);
             if (carry)
                 std::memcpy(slot, static_cast<char*>(h_in[prev]) + prev_full * row_bytes, carry);
-            const int64_t got = read(read_ctx, slot + carry, io);
+            // a C++ exception must not cross the C-ABI (nor end the process
+            // from this thread): a throwing source is a failed read
+            int64_t got;
+            try {
+                got = read(read_ctx, slot + carry, io);
+            } catch (...) {
+                got = -1;
+            }
             bool end = false;
             PsBlock b;
             b.slot = h;
@@ -1855,8 +1640,9 @@ int process_stream_pipelined(ppfg_plan p, uint64_t block_spectra, int zero_prime
                 carry = total % row_bytes;
                 prev = h;
                 prev_full = b.full;
-                if (static_cast<uint64_t>(got) < io) // short read: end of stream (source.eof())
-                    end = true;
+                // a short read is not the end: like the reference loop, read
+                // again — 0 ends the stream, < 0 is a source failure at the
+                // offset after the bytes already delivered (pipeline.hpp:138-143)
             }
             std::lock_guard<std::mutex> lk(sh.mu);
             if (!read_error && got > 0)
@@ -1900,7 +1686,13 @@ int process_stream_pipelined(ppfg_plan p, uint64_t block_spectra, int zero_prime
                 sh.fail_with(PPFG_CUDA_ERROR, "process_stream: D2H failed");
                 return;
             }
-            if (it.bytes && write(write_ctx, h_out[it.o], it.bytes) != 0) {
+            int wrc;
+            try {
+                wrc = it.bytes ? write(write_ctx, h_out[it.o], it.bytes) : 0;
+            } catch (...) {
+                wrc = 1;
+            }
+            if (wrc != 0) {
                 sh.fail_with(PPFG_IO_ERROR, "process_stream: sink write failed");
                 return;
             }
@@ -2106,8 +1898,11 @@ int ppfg_stream_open(ppfg_stream* out, ppfg_plan p, uint64_t block_spectra, int 
     }
     if (zero_prime) { // pipeline.hpp:110-111
         s->hist_rows = p->T - 1;
-        if (s->hist_rows)
-            cudaMemset(s->d_buf[0], 0, s->hist_rows * row_bytes);
+        if (s->hist_rows &&
+            cudaMemsetAsync(s->d_buf[0], 0, s->hist_rows * row_bytes, p->stream) != cudaSuccess) {
+            ppfg_stream_destroy(s);
+            return fail(PPFG_CUDA_ERROR, "stream_open: history priming failed");
+        }
     }
     *out = s;
     return PPFG_OK;

@@ -1,0 +1,23 @@
+// tab_fused_fft.cu — K3 with T = 1 and unit taps: the bit-exact TMA-fed FFT used by channelize_block.
+#include "tables_impl.cuh"
+
+namespace ppfg {
+
+std::vector<FusedEntry> fused_part_fft() {
+    return {
+        // T = 1 with unit taps: x*1 == x exactly, so these are bit-exact,
+        // TMA-fed, warp-specialised FFTs — channelize_block for 64 <= C <= 4096
+        // (C = 4096: 0.76 of roofline vs 0.69 for K2)
+        // (split-kernel T = 1 entries for C = 4096, 8192 and FP64 C = 4096 on
+        // 8-CTA clusters measured slower than K2 / the unfused path)
+        fused_entry<FusedCfg<6, 1, 0, false, 120, 80, 2, 3>>(),
+        fused_entry<FusedCfg<7, 1, 0, false, 120, 80, 2, 3>>(),
+        fused_entry<FusedCfg<8, 1, 0, false>>(),
+        fused_entry<FusedCfg<9, 1, 1, false>>(),
+        fused_entry<FusedCfg<10, 1, 2, false>>(),
+        fused_entry<FusedCfg<11, 1, 3, false, 160, 96, 3>>(),
+        fused_entry<FusedCfg<12, 1, 4, false, 160, 96, 2>>(),
+    };
+}
+
+} // namespace ppfg

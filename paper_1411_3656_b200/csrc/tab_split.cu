@@ -1,0 +1,38 @@
+// tab_split.cu — K3s split fused FIR+FFT kernels on thread-block clusters.
+#include "tables_impl.cuh"
+
+namespace ppfg {
+
+std::vector<FusedEntry> fused_part_split() {
+    return {
+        // thread-block clusters, FIR split by channel block and FFT by
+        // spectrum (fused_split.cuh) — for FIR state that does not fit one SM.
+        // preferred = taken by default: measured faster than FIR -> HBM -> FFT
+        // (round 1, 1 GiB inputs: C=1024 T=16 0.62 vs 0.32 of HBM roofline,
+        // T=32 0.41 vs 0.18, FP64 T=8 0.62 vs 0.42, FP64 T=16 0.40 vs 0.32,
+        // C=2048 0.51 vs 0.42, FP64 C=2048 0.47 vs 0.42, C=4096 0.43 vs 0.38;
+        // C=8192 0.29 vs 0.32 stays opt-in via PPFG_CLUSTER)
+        // (float4 twiddle tables where they measured faster: FAST C=1024
+        // T=16 0.62 vs 0.58, EXACT C=1024 T=16 0.40 vs 0.39, EXACT C=2048
+        // 0.47 vs 0.44; FAST C=2048/4096 gained 15-27 % from float2)
+        // (T=32 FAST: the unfused K1b FP32 FIR -> FFT measured 0.43 vs 0.42;
+        // FIR/FFT registers 136/120 instead of 152/104 at FAST C=1024 T=16
+        // 0.645 vs 0.619 and C=2048 0.688 vs 0.624 — not at C=4096 or FP64 C=2048;
+        // FP64 C=1024 T=8 with float4 twiddles 0.629 vs 0.620 over four A/B
+        // pairs; 4-CTA clusters 0.51, W=4 passes 0.44, FIR 168/88 0.44.
+        // Rejected in the same A/B: FAST C=4096 float4 0.42 / 8-CTA 0.31 vs
+        // 0.53; FP64 T=16 168/88 0.402 vs 0.403; FAST T=32 cluster 136/120
+        // 0.41, 168/88 0.42, 8-CTA 0.28 — all below unfused K1b 0.43)
+
+        split_entry<SplitCfg<10, 1, 16, false, 2, 5, 136, 120, 0, true>>(true),
+        split_entry<SplitCfg<10, 2, 32, false, 2, 5, 152, 104, 0, true>>(false),
+        split_entry<SplitCfg<10, 1, 8, true, 2, 5, 136, 120, 0, true>>(true),
+        split_entry<SplitCfg<10, 2, 16, true, 2, 5, 152, 104, 0, true>>(true),
+        split_entry<SplitCfg<11, 1, 8, false, 2, 5, 136, 120>>(true),
+        split_entry<SplitCfg<11, 2, 8, true, 2, 5, 152, 104, 0, true>>(true),
+        split_entry<SplitCfg<12, 2, 8, false>>(true),
+        split_entry<SplitCfg<13, 3, 8, false>>(false),
+    };
+}
+
+} // namespace ppfg

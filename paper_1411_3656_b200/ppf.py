@@ -218,6 +218,11 @@ class Plan:
     def kind(self):
         return self._lib.ppfg_fir_fft_kind(self._h)
 
+    @property
+    def kernel_name(self):
+        """The fir_fft kernel, as ncu names it (ppfg_fir_fft_kernel_name)."""
+        return self._lib.ppfg_fir_fft_kernel_name(self._h).decode()
+
     def close(self):
         if getattr(self, "_h", None):
             self._lib.ppfg_plan_destroy(self._h)

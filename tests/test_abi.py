@@ -92,6 +92,24 @@ def test_synth_host_is_deterministic_and_tone_plus_noise():
     assert abs(noise.mean()) < 0.05
 
 
+def test_oracle_synth_equals_the_library_generator():
+    """The reference arm of bench.py feeds the reference from the oracle's copy
+    of the synthetic generator (it must not load libppfg.so); its bytes must be
+    the product's (which the GPU tests pin to the device generator)."""
+    import oracle
+    from paper_1411_3656_b200 import ppf
+    for C, n, first, seed in [(1024, 1 << 18, 0, 1), (512, 12345, 777, 3), (8192, 5000, 10**12, 9)]:
+        a = oracle.port().synth(C, n, seed=seed, first_sample=first)
+        b = ppf.synth(C, n, seed=seed, first_sample=first)
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32)), (C, n, first)
+
+
+def test_kernel_name_is_exported():
+    from paper_1411_3656_b200 import _lib
+    lib = _lib.load()
+    assert lib.ppfg_fir_fft_kernel_name(None) == b""
+
+
 def test_new_entry_points_validate_arguments_without_a_gpu():
     """ppfg_multi_fir_fft_device and ppfg_process_stream reject null arguments
     before touching a device (status codes of include/ppfg.h)."""
