@@ -155,6 +155,11 @@ int ppfg_fir_fft_kind(ppfg_plan plan);
  * matched to profiles of exactly that kernel. Valid while the plan lives. */
 const char* ppfg_fir_fft_kernel_name(ppfg_plan plan);
 
+/* The device's theoretical HBM bandwidth in GB/s (2 x memory clock x bus
+ * width; device -1 = the current one): the default roofline denominator of
+ * the report layer (BenchmarkReport::roofline_frac). */
+int ppfg_device_hbm_gbs(int device, double* gb_per_sec);
+
 /* ---- single-row helpers (dft.hpp:39-66, 160-169), host memory ------------- */
 int ppfg_fft(const void* in, uint64_t n, void* out);        /* UNSUPPORTED_SIZE if n not 2^k */
 int ppfg_dft_naive(const void* in, uint64_t n, void* out);

@@ -37,6 +37,7 @@ SIGNATURES = {
     "ppfg_fir_fft_mean_power": (C.c_int, [vp, vp, u64, vp, C.c_int, vp]),
     "ppfg_fir_fft_kind": (C.c_int, [vp]),
     "ppfg_fir_fft_kernel_name": (C.c_char_p, [vp]),
+    "ppfg_device_hbm_gbs": (C.c_int, [C.c_int, dp]),
     "ppfg_fft": (C.c_int, [vp, u64, vp]),
     "ppfg_dft_naive": (C.c_int, [vp, u64, vp]),
     "ppfg_stream_open": (C.c_int, [C.POINTER(vp), vp, u64, C.c_int, C.c_int]),

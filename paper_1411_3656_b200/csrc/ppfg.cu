@@ -1163,6 +1163,22 @@ const char* ppfg_fir_fft_kernel_name(ppfg_plan p) {
     return p->fused_name.c_str();
 }
 
+int ppfg_device_hbm_gbs(int device, double* gbs) {
+    if (!gbs)
+        return fail(PPFG_CONFIG_ERROR, "device_hbm_gbs: null output");
+    *gbs = 0.0;
+    if (device < 0 && cudaGetDevice(&device) != cudaSuccess)
+        return fail(PPFG_NO_DEVICE, "ppfg: no current device");
+    int khz = 0, bits = 0;
+    if (cudaDeviceGetAttribute(&khz, cudaDevAttrMemoryClockRate, device) != cudaSuccess ||
+        cudaDeviceGetAttribute(&bits, cudaDevAttrGlobalMemoryBusWidth, device) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(PPFG_NO_DEVICE, "ppfg: cannot query the device memory system");
+    }
+    *gbs = 2.0 * static_cast<double>(khz) * 1e3 * static_cast<double>(bits) / 8.0 / 1e9;
+    return PPFG_OK;
+}
+
 int ppfg_fir_fft_kind(ppfg_plan p) {
     if (!p || !p->fused || (p->flags & PPFG_UNFUSED))
         return 0;
