@@ -86,6 +86,22 @@ PPFG_DEV void fft_prestages(float2 (&v)[1 << RLOG], const float4 (&twr)[RLOG > 0
     }
 }
 
+// FAST mode only: the same first two stages for R = 4 values (labels j,
+// j + N/4, j + N/2, j + 3N/4) with their exact twiddles 1 (stage 1), 1 and -i
+// (stage 2) applied as additions: 6 packed adds + 4 scalar adds instead of 4
+// butterflies (the reference multiplies by the f32-rounded table entries,
+// e.g. (6.1e-17, -1) for -i: a 1e-16-relative difference).
+PPFG_DEV void fft_prestages_trivial(float2 (&v)[4]) {
+    // stage 1 (label bit L-1): pairs (0, 2), (1, 3), twiddle 1
+    const float2 a0 = add2(v[0], v[2]), a2 = sub2(v[0], v[2]);
+    const float2 a1 = add2(v[1], v[3]), a3 = sub2(v[1], v[3]);
+    // stage 2 (label bit L-2): (0, 1) twiddle 1; (2, 3) twiddle -i: t = (hi.y, -hi.x)
+    v[0] = add2(a0, a1);
+    v[1] = sub2(a0, a1);
+    v[2] = make_float2(__fadd_rn(a2.x, a3.y), __fsub_rn(a2.y, a3.x));
+    v[3] = make_float2(__fsub_rn(a2.x, a3.y), __fadd_rn(a2.y, a3.x));
+}
+
 // ---- pass schedule: NP passes of near-equal width, widest first ------------------
 template <int L, int W>
 struct FftSchedule {

@@ -50,8 +50,20 @@ constexpr int ilcm(int a, int b) {
 }
 
 template <int L_, int T_, int RLOG_, bool EXACT_, int FIR_REGS_ = 160, int FFT_REGS_ = 96,
-          int PC_ = 4, int FFT_WG_ = 2, int NTILE_ = 2, bool TW4_ = false, int L2A_ = 0>
+          int PC_ = 4, int FFT_WG_ = 2, int NTILE_ = 2, bool TW4_ = false, int L2A_ = 0,
+          bool HS_ = false, bool TRIV_ = false>
 struct FusedCfg {
+    // HS: hand tiles over per FFT pass group instead of whole: the FIR role
+    // arrives on FULL[t][pg] as soon as the rows of pass group pg are written
+    // and waits on EMPTY[t][pg] just before writing them, so each FFT
+    // warpgroup starts on its rows while the FIR role is still filling the
+    // rest (needs one FIR group and an evenly split tile)
+    static constexpr bool HS = HS_;
+    // TRIV (FAST only): the FIR role's first two radix-2 stages use their
+    // trivial twiddles (1, 1, -i) as additions instead of the reference's
+    // multiplications by the rounded table values (6e-17 apart) — half the
+    // FMA-pipe work of the prestages; EXACT keeps the reference arithmetic
+    static constexpr bool TRIV = TRIV_;
     // L2A > 0: the producer also prefetches (cp.async.bulk.prefetch.L2) the
     // chunk L2A past the one it copies into the ring, so that chunk's bulk
     // copy later starts from L2 — lookahead without shared memory
@@ -108,6 +120,16 @@ struct FusedCfg {
     static_assert(FIR_REGS * NFIR + FFT_REGS * NFFT <= LAUNCH_REGS * NT, "register split");
     static_assert(SMEM <= 232448, "shared memory per CTA");
     static_assert(BU * B <= 32, "FIR unroll too large");
+    static_assert(!HS || (G == 1 && FFT_SPLIT && B % PROWS == 0), "per-group handoff layout");
+    static_assert(!HS || 1 + 2 * NTILE * PGROUPS + PGROUPS <= 16, "named barriers");
+    static_assert(!TRIV || (!EXACT && RLOG == 2), "trivial prestages: FAST, R = 4");
+    // named barrier ids (0 = __syncthreads): FULL[t][pg], EMPTY[t][pg], pass
+    // syncs per pass group (HS: per pass group; else one FULL / EMPTY per tile)
+    static constexpr int HPG = HS ? PGROUPS : 1;          // handoff groups per tile
+    static constexpr int HCOUNT = HS ? NFIR + PNT : NT;   // threads per handoff barrier
+    PPFG_HD static constexpr int bar_full(int t, int pg) { return 1 + t * HPG + pg; }
+    PPFG_HD static constexpr int bar_empty(int t, int pg) { return 1 + NTILE * HPG + t * HPG + pg; }
+    PPFG_HD static constexpr int bar_pass(int pg) { return 1 + 2 * NTILE * HPG + pg; }
 };
 
 // Output-row map for the final FFT pass: tile row r = g*B + i is output
@@ -204,14 +226,15 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
 #pragma unroll
         for (int k = 0; k < (POWER ? EL : 1); ++k)
             pacc[k] = 0.0;
+        const int hpg = Cfg::HS ? pg : 0;
         for (long long b = 0; b < n_batches; ++b) {
             const int t = static_cast<int>(b % Cfg::NTILE);
-            named_sync(1 + t, NT);
+            named_sync(Cfg::bar_full(t, hpg), Cfg::HCOUNT);
             Passes::run(nullptr, out,
                         tiles + (t * Cfg::TILE_ROWS + pg * PROWS) * Cfg::STRIDE, Cfg::STRIDE,
                         PROWS, OffsetRows{FusedRows{o0, o1, rpg, b * B, B}, pg * PROWS}, tw, ptid,
-                        SyncNamed{1 + 2 * Cfg::NTILE + pg, PNT}, pacc);
-            named_arrive(1 + Cfg::NTILE + t, NT);
+                        SyncNamed{Cfg::bar_pass(pg), PNT}, pacc);
+            named_arrive(Cfg::bar_empty(t, hpg), Cfg::HCOUNT);
         }
         if constexpr (POWER) {
             // every last-pass unit of this thread (tile rows ptid / UL +
@@ -306,8 +329,8 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
                 fence_proxy_async();
                 issue(b - 1 + PC);
             }
-            if (b >= Cfg::NTILE)
-                named_sync(1 + Cfg::NTILE + t, NT); // the FFT role has drained tile t
+            if (!Cfg::HS && b >= Cfg::NTILE)
+                named_sync(Cfg::bar_empty(t, 0), NT); // the FFT role has drained tile t
             if (have)
                 mbar_wait(full_g + slot, static_cast<uint32_t>((b / PC) & 1));
             const float2* chunk = ring_g + static_cast<size_t>(slot) * B * N + j;
@@ -317,6 +340,10 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
             // keeping the loads unpredicated lets the window rotate by renaming.
 #pragma unroll
             for (int i = 0; i < B; ++i) {
+                if constexpr (Cfg::HS) { // pass group i / PROWS has drained its rows of tile t
+                    if (i % Cfg::PROWS == 0 && b >= Cfg::NTILE)
+                        named_sync(Cfg::bar_empty(t, i / Cfg::PROWS), Cfg::HCOUNT);
+                }
                 float2 y[R];
 #pragma unroll
                 for (int k = 0; k < R; ++k) {
@@ -343,15 +370,23 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
                         y[k] = acc;
                     }
                 }
-                fft_prestages<L, RLOG>(y, twr);
+                if constexpr (Cfg::TRIV)
+                    fft_prestages_trivial(y);
+                else
+                    fft_prestages<L, RLOG>(y, twr);
 #pragma unroll
                 for (int k = 0; k < R; ++k)
                     tile[i * Cfg::STRIDE + sw(static_cast<unsigned>(k * NTG))] = y[k];
+                if constexpr (Cfg::HS) { // rows of pass group i / PROWS are written
+                    if ((i + 1) % Cfg::PROWS == 0)
+                        named_arrive(Cfg::bar_full(t, i / Cfg::PROWS), Cfg::HCOUNT);
+                }
             }
             __syncwarp();
             if (have && warp_leader)
                 mbar_arrive(empty_g + slot); // this warp is done with the chunk
-            named_arrive(1 + t, NT);         // tile t is full
+            if constexpr (!Cfg::HS)
+                named_arrive(Cfg::bar_full(t, 0), NT); // tile t is full
         }
     }
 }
