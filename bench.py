@@ -362,6 +362,81 @@ def time_steps(step, stream, steps):
     return ev0.elapsed_time(ev1) / 1e3, float(np.mean([a.elapsed_time(b) for a, b in per])) / 1e3
 
 
+def _median_time(fn, reps=5, warm=2):
+    """Median device time of fn() over reps (CUDA events on torch's current
+    stream, which the library's calls run on), after warm-ups."""
+    import torch
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    s = torch.cuda.current_stream()
+    ts = []
+    for _ in range(reps):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        fn()
+        b.record(s)
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b) / 1e3)
+    return float(np.median(ts))
+
+
+def config_points(dev, peak, long_bytes):
+    """Every BASELINE.json configuration on this GPU, device-resident (the
+    SKA headline is the main line): configs[0] cfg1 in full, the taps sweep
+    (C=1024, T=4..64) and channels sweep (T=8, C=64..8192) at 1 GiB, and the
+    long stream (C=1024, T=16) at `long_bytes` (64e9 = the whole stream on one
+    GPU). Per point FAST and EXACT fir_fft, and at each channel count the
+    bit-exact FFT alone (channelize_block) beside cuFFT (torch.fft.fft, the
+    comparison point, not bit-exact); detection (fused mean power) at
+    C=1024 T=8. Median of 5 after 2 warm-ups; frac = (in + out) / t / peak
+    (detection: in / t / peak, the fused pass being read-only)."""
+    import torch
+    from paper_1411_3656_b200 import ppf
+    pts = [("cfg1", 512, 8, 1 << 17)]
+    pts += [("taps", 1024, t, (1 << 30) // (1024 * 8)) for t in (4, 8, 16, 32, 64)]
+    pts += [("channels", c, 8, (1 << 30) // (c * 8)) for c in (64, 128, 256, 512, 1024, 2048, 4096, 8192)]
+    if long_bytes:
+        pts.append(("long16", 1024, 16, long_bytes // (1024 * 8)))
+    out = []
+    for name, C, T, S in pts:
+        try:
+            x = torch.empty((S, C), dtype=torch.complex64, device=dev)
+            y = torch.empty((S - T + 1, C), dtype=torch.complex64, device=dev)
+        except RuntimeError as e:  # out of memory: report, keep going
+            out.append({"config": name, "C": C, "T": T, "S_in": S, "error": str(e)[:120]})
+            torch.cuda.empty_cache()
+            continue
+        ppf.synth(C, S * C, seed=3, out=x)
+        coeffs = ppf.generate_prototype(C, T)
+        bi, bo = S * C * 8, (S - T + 1) * C * 8
+        r = {"config": name, "C": C, "T": T, "S_in": S, "bytes_in": bi}
+        for mode, flags in (("fast", ppf.FAST), ("exact", ppf.EXACT)):
+            with ppf.Plan(C, T, coeffs, flags=flags) as p:
+                t = _median_time(lambda: p.fir_fft(x, out=y))
+                r[mode] = {"ms": t * 1e3, "input_gbps": bi / t / 1e9,
+                           "x_realtime": bi / t / SKA_RATE, "frac": (bi + bo) / t / 1e9 / peak,
+                           "kernel": p.kernel_name}
+        if name == "channels":
+            with ppf.Plan(C, 0) as p:
+                t = _median_time(lambda: p.channelize(y, out=y))
+            tc = _median_time(lambda: torch.fft.fft(y, dim=1))
+            r["fft_only"] = {"ms": t * 1e3, "frac": 2 * bo / t / 1e9 / peak,
+                             "what": "channelize_block, bit-exact radix-2, in place"}
+            r["cufft"] = {"ms": tc * 1e3, "frac": 2 * bo / tc / 1e9 / peak,
+                          "what": "torch.fft.fft (cuFFT), comparison only, not bit-exact"}
+        if name == "taps" and T == 8:
+            with ppf.Plan(C, T, coeffs, flags=ppf.FAST) as p:
+                t = _median_time(lambda: p.fir_fft_mean_power(x))
+            r["detect"] = {"ms": t * 1e3, "input_gbps": bi / t / 1e9, "frac_read_only": bi / t / 1e9 / peak,
+                           "what": "fir_fft_mean_power (cmd_inspect, cli.hpp:307-317), FAST"}
+        out.append(r)
+        del x, y
+        torch.cuda.empty_cache()
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -378,6 +453,9 @@ def main():
     ap.add_argument("--no-exact", action="store_true", help="skip the EXACT-mode sub-record")
     ap.add_argument("--no-parity", action="store_true", help="skip the whole-output check")
     ap.add_argument("--parity-chunk-mib", type=int, default=512)
+    ap.add_argument("--no-configs", action="store_true", help="skip the BASELINE config sweep")
+    ap.add_argument("--long-gb", type=float, default=64.0,
+                    help="long-stream config size on one GPU (GB of input; 0 = skip)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -537,6 +615,18 @@ def main():
                              "sample": f"{sample} spectra, ppf_fir_optimized one-shot "
                                        f"(fir.hpp:158-212), best of 3"}}
 
+    # ---- every BASELINE.json configuration (N=1 rank 0): the sweeps ----
+    configs = None
+    if rank == 0 and world == 1 and not args.no_configs:
+        del x, y
+        torch.cuda.empty_cache()
+        t0 = time.perf_counter()
+        configs = {"points": config_points(dev, peak, int(args.long_gb * 1e9)),
+                   "peak_gbps": peak, "seconds": None,
+                   "timing": "median of 5 after 2 warm-ups, CUDA events, device-resident; "
+                             "1 GiB points, cfg1 and long16 at their full size"}
+        configs["seconds"] = time.perf_counter() - t0
+
     if rank == 0:
         kind = plan.kind
         kname = plan.kernel_name
@@ -558,7 +648,7 @@ def main():
             "x_realtime": value * 1e9 / SKA_RATE,
             "config": {"workload": desc, "n_channels": C, "n_taps": T,
                        "n_spectra_in_per_gpu": ic, "bytes_in_per_gpu": bytes_in,
-                       "mode": args.mode, "kernel": ["unfused", "fused-fp32", "fused-fp64", "cluster-fp32", "cluster-fp64"][kind],
+                       "mode": args.mode, "kernel": ["unfused", "fused-fp32", "fused-fp64", "cluster-fp32", "cluster-fp64", "tiny-fp32", "tiny-fp64"][kind],
                        "l2": "inputs >> 126 MB L2 (no flush needed)", "parallelism": f"shard{world}"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
@@ -569,6 +659,7 @@ def main():
             "exact": exact,
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "configs": configs,
             "clocks": clocks,
             "gpu_launches": int(launches),
         }

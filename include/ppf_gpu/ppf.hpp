@@ -29,6 +29,8 @@
 #include <fstream>
 #include <functional>
 #include <istream>
+#include <list>
+#include <mutex>
 #include <numbers>
 #include <optional>
 #include <ostream>
@@ -301,6 +303,82 @@ private:
 };
 
 namespace detail {
+// Process-wide cache of device plans for the one-shot calls (ppf_fir_*,
+// channelize_block): the reference API is stateless and a caller looping per
+// block (bench.hpp:129-150, pipeline.hpp:121-136) would otherwise pay plan
+// creation — tap / twiddle uploads, streams, events — and a fresh pinned
+// staging area on every call. Plans are keyed by (device, C, T, flags,
+// coefficient values); a plan is leased to one call at a time (plans are not
+// thread-safe), concurrent callers get their own, and at most kMaxIdle idle
+// plans are kept (least recently used dropped first).
+class PlanCache {
+public:
+    struct Key {
+        int device = 0;
+        std::size_t n_channels = 0, n_taps = 0;
+        std::uint32_t flags = 0;
+        std::vector<double> values;
+        bool operator==(const Key& o) const {
+            return device == o.device && n_channels == o.n_channels && n_taps == o.n_taps &&
+                   flags == o.flags && values == o.values;
+        }
+    };
+    class Lease {
+    public:
+        Lease(PlanCache* c, Key k, ppfg_plan p) : c_(c), k_(std::move(k)), p_(p) {}
+        Lease(const Lease&) = delete;
+        Lease& operator=(const Lease&) = delete;
+        ~Lease() { c_->give_back(std::move(k_), p_); }
+        ppfg_plan get() const { return p_; }
+
+    private:
+        PlanCache* c_;
+        Key k_;
+        ppfg_plan p_;
+    };
+    static PlanCache& instance() {
+        static PlanCache* c = new PlanCache(); // leaked on purpose: no exit-order issues
+        return *c;
+    }
+    Lease acquire(std::size_t n_channels, std::size_t n_taps, const double* values,
+                  std::uint32_t flags = PPFG_EXACT) {
+        Key k;
+        check(ppfg_current_device(&k.device));
+        k.n_channels = n_channels;
+        k.n_taps = n_taps;
+        k.flags = flags;
+        if (n_taps)
+            k.values.assign(values, values + n_channels * n_taps);
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            for (auto it = idle_.begin(); it != idle_.end(); ++it) {
+                if (it->first == k) {
+                    ppfg_plan p = it->second;
+                    idle_.erase(it);
+                    return Lease(this, std::move(k), p);
+                }
+            }
+        }
+        ppfg_plan p = nullptr;
+        check(ppfg_plan_create(&p, n_channels, n_taps, n_taps ? k.values.data() : nullptr, flags,
+                               k.device));
+        return Lease(this, std::move(k), p);
+    }
+
+private:
+    static constexpr std::size_t kMaxIdle = 8;
+    void give_back(Key k, ppfg_plan p) {
+        std::lock_guard<std::mutex> lk(mu_);
+        idle_.emplace_front(std::move(k), p);
+        while (idle_.size() > kMaxIdle) {
+            ppfg_plan_destroy(idle_.back().second);
+            idle_.pop_back();
+        }
+    }
+    std::mutex mu_;
+    std::list<std::pair<Key, ppfg_plan>> idle_; // most recently used first
+};
+
 inline void check_fir_preconditions(const SampleBlock& input, const FilterCoefficients& coeffs) {
     input.validate();
     if (coeffs.n_channels == 0 || coeffs.n_taps == 0 ||
@@ -319,7 +397,7 @@ inline FilteredBlock run_fir(const SampleBlock& input, const FilterCoefficients&
     out.n_channels = input.n_channels;
     out.n_spectra_out = input.n_spectra() - coeffs.n_taps + 1;
     out.spectra.resize(out.n_spectra_out * out.n_channels);
-    Plan p(coeffs.n_channels, coeffs.n_taps, coeffs.values.data());
+    auto p = PlanCache::instance().acquire(coeffs.n_channels, coeffs.n_taps, coeffs.values.data());
     auto fn = reference_order ? ppfg_fir_reference_order : ppfg_fir;
     detail::check(fn(p.get(), input.samples.data(), input.n_spectra(), out.spectra.data(),
                      PPFG_MEM_HOST, nullptr));
@@ -406,7 +484,7 @@ inline ChannelizedOutput channelize_block(const FilteredBlock& filtered, bool ff
         throw unsupported_size_error(
             "channelize_block: non-power-of-two channel count with fallback disabled");
     out.bins.resize(filtered.spectra.size());
-    Plan p(filtered.n_channels, 0, nullptr);
+    auto p = detail::PlanCache::instance().acquire(filtered.n_channels, 0, nullptr);
     detail::check(ppfg_channelize(p.get(), filtered.spectra.data(), out.n_spectra, out.bins.data(),
                                   fft_fallback ? 1 : 0, PPFG_MEM_HOST, nullptr));
     return out;

@@ -148,7 +148,7 @@ int ppfg_fir_fft_mean_power(ppfg_plan plan, const void* in, uint64_t n_spectra_i
 
 /* Which kernel ppfg_fir_fft will run for this plan: 0 = unfused FIR+FFT,
  * 1 = fused FP32-FIR, 2 = fused FP64 (bit-exact) FIR, 3 / 4 = the cluster
- * versions of 1 / 2. */
+ * versions of 1 / 2, 5 / 6 = the warp-level tiny-C (2..32) versions of 1 / 2. */
 int ppfg_fir_fft_kind(ppfg_plan plan);
 /* The kernel ppfg_fir_fft launches for this plan, named the way ncu prints it
  * ("fused_fir_fft_kernel<FusedCfg<10, 8, 2, 0, ...>>"), so measurements can be
@@ -159,6 +159,13 @@ const char* ppfg_fir_fft_kernel_name(ppfg_plan plan);
  * width; device -1 = the current one): the default roofline denominator of
  * the report layer (BenchmarkReport::roofline_frac). */
 int ppfg_device_hbm_gbs(int device, double* gb_per_sec);
+
+/* Host memcpy split over the library's small pool of copy threads (the same
+ * pool that stages pageable buffers for the host-memory entry points): for
+ * the drop-in's host-side bookkeeping (carry_history, pipeline.hpp:55-73). */
+int ppfg_host_copy(void* dst, const void* src, uint64_t bytes);
+/* The calling thread's current CUDA device (plan caches key on it). */
+int ppfg_current_device(int* device);
 
 /* ---- single-row helpers (dft.hpp:39-66, 160-169), host memory ------------- */
 int ppfg_fft(const void* in, uint64_t n, void* out);        /* UNSUPPORTED_SIZE if n not 2^k */

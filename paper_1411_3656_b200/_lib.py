@@ -38,6 +38,8 @@ SIGNATURES = {
     "ppfg_fir_fft_kind": (C.c_int, [vp]),
     "ppfg_fir_fft_kernel_name": (C.c_char_p, [vp]),
     "ppfg_device_hbm_gbs": (C.c_int, [C.c_int, dp]),
+    "ppfg_host_copy": (C.c_int, [vp, vp, u64]),
+    "ppfg_current_device": (C.c_int, [C.POINTER(C.c_int)]),
     "ppfg_fft": (C.c_int, [vp, u64, vp]),
     "ppfg_dft_naive": (C.c_int, [vp, u64, vp]),
     "ppfg_stream_open": (C.c_int, [C.POINTER(vp), vp, u64, C.c_int, C.c_int]),

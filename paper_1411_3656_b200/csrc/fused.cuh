@@ -53,11 +53,12 @@ template <int L_, int T_, int RLOG_, bool EXACT_, int FIR_REGS_ = 160, int FFT_R
           int PC_ = 4, int FFT_WG_ = 2, int NTILE_ = 2, bool TW4_ = false, int L2A_ = 0,
           bool HS_ = false, bool TRIV_ = false>
 struct FusedCfg {
-    // HS: hand tiles over per FFT pass group instead of whole: the FIR role
-    // arrives on FULL[t][pg] as soon as the rows of pass group pg are written
-    // and waits on EMPTY[t][pg] just before writing them, so each FFT
+    // HS: hand tiles over per FFT pass group instead of whole: a FIR thread
+    // arrives on FULL[t][pg] as soon as it has written its rows of pass group
+    // pg and waits on EMPTY[t][pg] just before writing them, so each FFT
     // warpgroup starts on its rows while the FIR role is still filling the
-    // rest (needs one FIR group and an evenly split tile)
+    // rest (needs an evenly split tile; with several FIR groups a pass
+    // group's barrier counts the groups that write its rows)
     static constexpr bool HS = HS_;
     // TRIV (FAST only): the FIR role's first two radix-2 stages use their
     // trivial twiddles (1, 1, -i) as additions instead of the reference's
@@ -120,13 +121,18 @@ struct FusedCfg {
     static_assert(FIR_REGS * NFIR + FFT_REGS * NFFT <= LAUNCH_REGS * NT, "register split");
     static_assert(SMEM <= 232448, "shared memory per CTA");
     static_assert(BU * B <= 32, "FIR unroll too large");
-    static_assert(!HS || (G == 1 && FFT_SPLIT && B % PROWS == 0), "per-group handoff layout");
+    static_assert(!HS || FFT_SPLIT, "per-pass-group handoff needs an evenly split tile");
     static_assert(!HS || 1 + 2 * NTILE * PGROUPS + PGROUPS <= 16, "named barriers");
     static_assert(!TRIV || (!EXACT && RLOG == 2), "trivial prestages: FAST, R = 4");
     // named barrier ids (0 = __syncthreads): FULL[t][pg], EMPTY[t][pg], pass
     // syncs per pass group (HS: per pass group; else one FULL / EMPTY per tile)
     static constexpr int HPG = HS ? PGROUPS : 1;          // handoff groups per tile
-    static constexpr int HCOUNT = HS ? NFIR + PNT : NT;   // threads per handoff barrier
+    // threads on pass group pg's handoff barriers: the FIR groups writing any
+    // of its rows [pg*PROWS, (pg+1)*PROWS) (group g writes rows g*B .. g*B+B-1)
+    // and the pass group's own threads; the whole CTA without HS
+    PPFG_HD static constexpr int hcount(int pg) {
+        return HS ? NTG * (((pg + 1) * PROWS - 1) / B - (pg * PROWS) / B + 1) + PNT : NT;
+    }
     PPFG_HD static constexpr int bar_full(int t, int pg) { return 1 + t * HPG + pg; }
     PPFG_HD static constexpr int bar_empty(int t, int pg) { return 1 + NTILE * HPG + t * HPG + pg; }
     PPFG_HD static constexpr int bar_pass(int pg) { return 1 + 2 * NTILE * HPG + pg; }
@@ -229,12 +235,12 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
         const int hpg = Cfg::HS ? pg : 0;
         for (long long b = 0; b < n_batches; ++b) {
             const int t = static_cast<int>(b % Cfg::NTILE);
-            named_sync(Cfg::bar_full(t, hpg), Cfg::HCOUNT);
+            named_sync(Cfg::bar_full(t, hpg), Cfg::hcount(hpg));
             Passes::run(nullptr, out,
                         tiles + (t * Cfg::TILE_ROWS + pg * PROWS) * Cfg::STRIDE, Cfg::STRIDE,
                         PROWS, OffsetRows{FusedRows{o0, o1, rpg, b * B, B}, pg * PROWS}, tw, ptid,
                         SyncNamed{Cfg::bar_pass(pg), PNT}, pacc);
-            named_arrive(Cfg::bar_empty(t, hpg), Cfg::HCOUNT);
+            named_arrive(Cfg::bar_empty(t, hpg), Cfg::hcount(hpg));
         }
         if constexpr (POWER) {
             // every last-pass unit of this thread (tile rows ptid / UL +
@@ -340,9 +346,10 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
             // keeping the loads unpredicated lets the window rotate by renaming.
 #pragma unroll
             for (int i = 0; i < B; ++i) {
-                if constexpr (Cfg::HS) { // pass group i / PROWS has drained its rows of tile t
-                    if (i % Cfg::PROWS == 0 && b >= Cfg::NTILE)
-                        named_sync(Cfg::bar_empty(t, i / Cfg::PROWS), Cfg::HCOUNT);
+                if constexpr (Cfg::HS) { // tile row g*B+i's pass group has drained tile t
+                    const int r = g * B + i;
+                    if ((i == 0 || r % Cfg::PROWS == 0) && b >= Cfg::NTILE)
+                        named_sync(Cfg::bar_empty(t, r / Cfg::PROWS), Cfg::hcount(r / Cfg::PROWS));
                 }
                 float2 y[R];
 #pragma unroll
@@ -377,9 +384,10 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
 #pragma unroll
                 for (int k = 0; k < R; ++k)
                     tile[i * Cfg::STRIDE + sw(static_cast<unsigned>(k * NTG))] = y[k];
-                if constexpr (Cfg::HS) { // rows of pass group i / PROWS are written
-                    if ((i + 1) % Cfg::PROWS == 0)
-                        named_arrive(Cfg::bar_full(t, i / Cfg::PROWS), Cfg::HCOUNT);
+                if constexpr (Cfg::HS) { // this group's rows of the pass group are written
+                    const int r = g * B + i;
+                    if (i == B - 1 || (r + 1) % Cfg::PROWS == 0)
+                        named_arrive(Cfg::bar_full(t, r / Cfg::PROWS), Cfg::hcount(r / Cfg::PROWS));
                 }
             }
             __syncwarp();

@@ -670,9 +670,39 @@ bool launch_fir_fast(ppfg_plan p, const float2* din, uint64_t S_in, float2* dout
 // takes the plain-load kernels instead
 bool aligned16(const void* ptr) { return reinterpret_cast<uintptr_t>(ptr) % 16 == 0; }
 
+// K6: tiny power-of-two C (2..32), one warp-level kernel (tiny.cuh). Lane
+// groups of C lanes take contiguous time segments (a multiple of T spectra,
+// enough segments for ~4 waves of 48 warps per SM).
+bool launch_tiny(ppfg_plan p, const float2* din, uint64_t S_in, float2* dout, cudaStream_t st, int* rc) {
+    if (p->L < 1 || p->L > 5 || (p->flags & PPFG_UNFUSED))
+        return false;
+    const KernelFn fn = tiny_table(p->L, static_cast<int>(p->T), !(p->flags & PPFG_FAST));
+    if (!fn)
+        return false;
+    const uint64_t T = p->T, S_out = S_in - T + 1;
+    const uint64_t groups_per_warp = 32 >> p->L;
+    const uint64_t target = static_cast<uint64_t>(p->num_sms) * 48 * 4 * groups_per_warp;
+    uint64_t seg = std::max<uint64_t>(cdiv(S_out, target), std::min<uint64_t>(S_out, 4 * T));
+    seg = cdiv(seg, T) * T;
+    const long long n_tasks = static_cast<long long>(cdiv(S_out, seg));
+    const uint64_t warps = cdiv(static_cast<uint64_t>(n_tasks), groups_per_warp);
+    long long S_in_ll = static_cast<long long>(S_in), S_out_ll = static_cast<long long>(S_out);
+    int seg_i = static_cast<int>(seg);
+    long long nt = n_tasks;
+    void* args[] = {&din, &dout, &S_in_ll, &S_out_ll, &p->d_taps, &p->d_tw, &seg_i, &nt};
+    *rc = cudaLaunchKernel(fn, dim3(static_cast<unsigned>(cdiv(warps * 32, 256))), dim3(256), args, 0, st) ==
+                  cudaSuccess
+              ? check_launch("tiny fused fir+fft kernel")
+              : fail(PPFG_CUDA_ERROR, "tiny fused fir+fft kernel: launch failed");
+    return true;
+}
+
 int launch_fir_fft(ppfg_plan p, const float2* din, uint64_t S_in, float2* dout, cudaStream_t st) {
     if (p->fused && !(p->flags & PPFG_UNFUSED) && aligned16(din))
         return launch_fused(p, din, S_in, dout, st);
+    int rc_tiny = PPFG_OK;
+    if (launch_tiny(p, din, S_in, dout, st, &rc_tiny))
+        return rc_tiny;
     int rc = PPFG_OK;
     if ((p->flags & PPFG_FAST) && launch_fir_fast(p, din, S_in, dout, st, &rc)) {
         PPFG_TRY(rc);
@@ -784,6 +814,96 @@ int run_mean_power(ppfg_plan p, bool fused, const void* in, uint64_t n_rows, dou
     return rc;
 }
 
+// ------------------------------------------------------ host copy pool
+// Pageable callers (the reference API hands over std::vectors) pay a host
+// copy into / out of pinned staging per call; one core copies ~10-15 GB/s,
+// below PCIe, so large copies are split over a small process-wide pool of
+// worker threads (they also take the first-touch page faults of freshly
+// allocated output vectors in parallel).
+class CopyPool {
+public:
+    static CopyPool& get() {
+        static CopyPool* p = new CopyPool(); // never destroyed: no teardown-order issues
+        return *p;
+    }
+    void copy(void* dst, const void* src, size_t bytes) {
+        constexpr size_t kPiece = size_t(2) << 20;
+        if (bytes < 2 * kPiece || n_workers_ == 0) {
+            std::memcpy(dst, src, bytes);
+            return;
+        }
+        std::lock_guard<std::mutex> one(job_mu_); // one parallel copy at a time
+        const size_t parts = std::min<size_t>(n_workers_ + 1, bytes / kPiece);
+        job_dst_ = static_cast<char*>(dst);
+        job_src_ = static_cast<const char*>(src);
+        job_bytes_ = bytes;
+        job_per_ = (bytes / parts + 63) & ~size_t(63);
+        job_parts_ = parts;
+        done_.store(0, std::memory_order_relaxed);
+        const uint64_t g = ++gen_;
+        // publish: the job fields happen-before any claim of generation g
+        next_.store(g << 32, std::memory_order_release);
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            wake_ = g;
+        }
+        cv_.notify_all();
+        work(g);
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_done_.wait(lk, [&] { return done_.load(std::memory_order_acquire) == parts; });
+    }
+
+private:
+    CopyPool() {
+        const unsigned hw = std::thread::hardware_concurrency();
+        n_workers_ = hw > 2 ? std::min(hw - 1, 7u) : 0u;
+        for (unsigned i = 0; i < n_workers_; ++i)
+            std::thread([this] { loop(); }).detach();
+    }
+    // claim parts of generation g (index in the low 32 bits of next_) until
+    // none is left; a part claimed keeps the job (and its fields) alive
+    void work(uint64_t g) {
+        size_t finished = 0;
+        for (;;) {
+            uint64_t v = next_.load(std::memory_order_acquire);
+            if ((v >> 32) != g || (v & 0xffffffffu) >= job_parts_)
+                break;
+            if (!next_.compare_exchange_weak(v, v + 1, std::memory_order_acq_rel))
+                continue;
+            const size_t o = (v & 0xffffffffu) * job_per_;
+            if (o < job_bytes_)
+                std::memcpy(job_dst_ + o, job_src_ + o, std::min(job_per_, job_bytes_ - o));
+            ++finished;
+        }
+        if (finished && done_.fetch_add(finished, std::memory_order_acq_rel) + finished == job_parts_) {
+            std::lock_guard<std::mutex> lk(mu_);
+            cv_done_.notify_all();
+        }
+    }
+    void loop() {
+        uint64_t seen = 0;
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return wake_ != seen; });
+                seen = wake_;
+            }
+            work(seen);
+        }
+    }
+    unsigned n_workers_ = 0;
+    std::mutex job_mu_, mu_;
+    std::condition_variable cv_, cv_done_;
+    uint64_t gen_ = 0, wake_ = 0;
+    char* job_dst_ = nullptr;
+    const char* job_src_ = nullptr;
+    size_t job_bytes_ = 0, job_per_ = 0, job_parts_ = 0;
+    std::atomic<uint64_t> next_{0};
+    std::atomic<size_t> done_{0};
+};
+
+void host_copy(void* dst, const void* src, size_t bytes) { CopyPool::get().copy(dst, src, bytes); }
+
 // ------------------------------------------------------ host-mode pipeline
 bool is_pinned(const void* ptr) {
     cudaPointerAttributes a{};
@@ -842,6 +962,7 @@ int launch_op(ppfg_plan p, Op op, const float2* din, uint64_t n_in_rows, float2*
 }
 
 constexpr size_t kChunkBytes = size_t(64) << 20;
+constexpr size_t kPageableChunkBytes = size_t(8) << 20;
 
 // Host buffers -> chunked, double-buffered H2D | kernel | D2H on three streams.
 // `halo` input rows overlap between chunks (T-1 for the FIR, 0 for the FFT);
@@ -851,11 +972,14 @@ int run_host(ppfg_plan p, Op op, const void* hin, uint64_t n_in_rows, void* hout
     const uint64_t n_out_rows = n_in_rows - halo;
     if (n_out_rows == 0)
         return PPFG_OK;
+    const bool pin_in = is_pinned(hin), pin_out = is_pinned(hout);
+    // pageable buffers: smaller chunks, so the host staging copy of chunk i+1
+    // overlaps the PCIe transfers and the kernel of chunk i
+    const uint64_t chunk_bytes = pin_in && pin_out ? kChunkBytes : kPageableChunkBytes;
     const uint64_t chunk = std::max<uint64_t>(1, std::min<uint64_t>(n_out_rows,
-                                                                   kChunkBytes / row_bytes));
+                                                                   chunk_bytes / row_bytes));
     PPFG_TRY(grow_device(p->d_in, &p->d_in_bytes, (chunk + halo) * row_bytes));
     PPFG_TRY(grow_device(p->d_out, &p->d_out_bytes, chunk * row_bytes));
-    const bool pin_in = is_pinned(hin), pin_out = is_pinned(hout);
     if (!pin_in)
         PPFG_TRY(grow_pinned(p->h_in, &p->h_in_bytes, (chunk + halo) * row_bytes));
     if (!pin_out)
@@ -869,7 +993,7 @@ int run_host(ppfg_plan p, Op op, const void* hin, uint64_t n_in_rows, void* hout
         const uint64_t o = i * chunk, n = std::min(chunk, n_out_rows - o);
         PPFG_CUDA(cudaEventSynchronize(p->ev_d2h[b]));
         if (!pin_out)
-            std::memcpy(dst + o * row_bytes, p->h_out[b], n * row_bytes);
+            host_copy(dst + o * row_bytes, p->h_out[b], n * row_bytes);
         return PPFG_OK;
     };
     for (uint64_t i = 0; i < n_chunks; ++i) {
@@ -887,7 +1011,7 @@ int run_host(ppfg_plan p, Op op, const void* hin, uint64_t n_in_rows, void* hout
         const void* h2d_src = src + o * row_bytes;
         if (!pin_in) {
             PPFG_CUDA(cudaEventSynchronize(p->ev_h2d[b])); // staging buffer reusable
-            std::memcpy(p->h_in[b], src + o * row_bytes, in_bytes);
+            host_copy(p->h_in[b], src + o * row_bytes, in_bytes);
             h2d_src = p->h_in[b];
         }
         PPFG_CUDA(cudaMemcpyAsync(p->d_in[b], h2d_src, in_bytes, cudaMemcpyHostToDevice,
@@ -1158,9 +1282,29 @@ void* ppfg_plan_stream(ppfg_plan plan) { return plan ? plan->stream : nullptr; }
 const char* ppfg_fir_fft_kernel_name(ppfg_plan p) {
     if (!p)
         return "";
+    if (!(p->flags & PPFG_UNFUSED) && p->L >= 1 && p->L <= 5 && p->T > 0 &&
+        tiny_table(p->L, static_cast<int>(p->T), !(p->flags & PPFG_FAST)))
+        return p->flags & PPFG_FAST ? "fused_tiny_kernel (FP32 FIR)" : "fused_tiny_kernel (FP64 FIR)";
     if (!p->fused || (p->flags & PPFG_UNFUSED))
         return "unfused (FIR kernel + FFT kernel)";
     return p->fused_name.c_str();
+}
+
+int ppfg_host_copy(void* dst, const void* src, uint64_t bytes) {
+    if (bytes && (!dst || !src))
+        return fail(PPFG_CONFIG_ERROR, "host_copy: null buffer");
+    host_copy(dst, src, bytes);
+    return PPFG_OK;
+}
+
+int ppfg_current_device(int* device) {
+    if (!device)
+        return fail(PPFG_CONFIG_ERROR, "current_device: null output");
+    if (cudaGetDevice(device) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(PPFG_NO_DEVICE, "ppfg: no current device");
+    }
+    return PPFG_OK;
 }
 
 int ppfg_device_hbm_gbs(int device, double* gbs) {
@@ -1180,6 +1324,9 @@ int ppfg_device_hbm_gbs(int device, double* gbs) {
 }
 
 int ppfg_fir_fft_kind(ppfg_plan p) {
+    if (p && !(p->flags & PPFG_UNFUSED) && p->L >= 1 && p->L <= 5 && p->T > 0 &&
+        tiny_table(p->L, static_cast<int>(p->T), !(p->flags & PPFG_FAST)))
+        return p->flags & PPFG_FAST ? 5 : 6;
     if (!p || !p->fused || (p->flags & PPFG_UNFUSED))
         return 0;
     return (p->fused->exact ? 2 : 1) + (p->fused->q > 1 ? 2 : 0);

@@ -9,6 +9,22 @@
 namespace ppfg {
 
 std::vector<FusedEntry> fused_part_main() {
+    // Round 2: per-pass-group tile handoff (FusedCfg HS, the 12th argument)
+    // wherever it applies (one FIR group, evenly split tile) and measured
+    // faster (1 GiB, fraction of the measured HBM peak, two A/B rounds):
+    // C=1024 T=8 FAST 0.81 -> 0.93 (6.5 GB SKA bench 0.868 -> 0.994; with the
+    // trivial-twiddle prestages TRIV as well 1.001), C=1024 T=4 FAST (with
+    // TRIV) 0.848 -> 0.856, EXACT 0.76 -> 0.80, C=512 T=16 0.755 -> 0.82,
+    // EXACT C=512 T=8 0.68 -> 0.77, EXACT C=256 T=16 0.53 -> 0.56, C=256 T=32
+    // 0.605 -> 0.635. Not on the T = 1 FFT entries (C=256 0.90 -> 0.85,
+    // C=1024 0.884 -> 0.868) nor TRIV there (channelize_block must stay
+    // bit-exact). With several FIR groups per CTA (C <= 512 at R = 4,
+    // C <= 256 at R = 2) HS helped every EXACT shape (C=128 T=8 0.71 -> 0.75,
+    // C=256 0.756 -> 0.769, C=512 T=4 0.85 -> 0.90), FAST at T >= 16 (C=256
+    // T=16 0.84 -> 0.86, C=128 T=32 0.626 -> 0.644), C=64 T=8 (0.88 -> 0.92)
+    // and C=256 T=4 (0.794 -> 0.81), but not FAST C=128..512 at T=8 (cfg1
+    // C=512: 0.90 -> 0.82) nor C=512 T=4 (0.89 -> 0.85): those keep
+    // whole-tile handoff.
     return {
         // (float4 twiddle tables where they measured faster than float2:
         // C=1024 T=8 FAST 0.86 vs 0.85 at the SKA size, C=512 EXACT 0.68 vs
@@ -19,18 +35,18 @@ std::vector<FusedEntry> fused_part_main() {
         // 0.90 — but not at C=1024 T=4: 0.83 vs 0.86; FIR/FFT registers
         // 136/120 instead of 160/96 at C=512 T=16 0.76 vs 0.72 and FP64
         // C=1024 T=4 0.762 vs 0.753)
-        fused_entry<FusedCfg<10, 8, 2, false, 120, 80, 2, 3, 2, true, 1>>(),
+        fused_entry<FusedCfg<10, 8, 2, false, 120, 80, 2, 3, 2, true, 1, true, true>>(),
         fused_entry<FusedCfg<9, 8, 2, false, 120, 80, 2, 3>>(),
         fused_entry<FusedCfg<8, 8, 2, false, 120, 80, 2, 3>>(),
         fused_entry<FusedCfg<7, 8, 2, false, 120, 80, 2, 3>>(),
-        fused_entry<FusedCfg<6, 8, 1, false, 120, 80, 2, 3, 2, true>>(),
-        fused_entry<FusedCfg<10, 4, 2, false>>(),
-        fused_entry<FusedCfg<9, 16, 1, false, 136, 120>>(),
-        fused_entry<FusedCfg<9, 8, 1, true, 160, 96, 4, 2, 2, true>>(),
-        fused_entry<FusedCfg<8, 8, 1, true, 160, 96, 4, 2, 2, true>>(),
-        fused_entry<FusedCfg<7, 8, 1, true, 160, 96, 4, 2, 2, true>>(),
-        fused_entry<FusedCfg<6, 8, 1, true, 160, 96, 4, 2, 2, true>>(),
-        fused_entry<FusedCfg<10, 4, 2, true, 136, 120>>(),
+        fused_entry<FusedCfg<6, 8, 1, false, 120, 80, 2, 3, 2, true, 0, true>>(),
+        fused_entry<FusedCfg<10, 4, 2, false, 160, 96, 4, 2, 2, false, 0, true, true>>(),
+        fused_entry<FusedCfg<9, 16, 1, false, 136, 120, 4, 2, 2, false, 0, true>>(),
+        fused_entry<FusedCfg<9, 8, 1, true, 160, 96, 4, 2, 2, true, 0, true>>(),
+        fused_entry<FusedCfg<8, 8, 1, true, 160, 96, 4, 2, 2, true, 0, true>>(),
+        fused_entry<FusedCfg<7, 8, 1, true, 160, 96, 4, 2, 2, true, 0, true>>(),
+        fused_entry<FusedCfg<6, 8, 1, true, 160, 96, 4, 2, 2, true, 0, true>>(),
+        fused_entry<FusedCfg<10, 4, 2, true, 136, 120, 4, 2, 2, false, 0, true>>(),
     };
 }
 

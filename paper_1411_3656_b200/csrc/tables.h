@@ -73,5 +73,8 @@ FirTmaEntry fir_tma_table(int T);   // K1t, tab_fir.cu
 FirTmaEntry fir_fast_table(int T);  // K1f, tab_fir.cu
 FirBlkEntry fir_blk_table(int T, bool exact); // K1b, tab_fir_blk.cu
 FirEntry fir_table(int T);          // K1, tab_fir.cu
+// K6 fused FIR+FFT for C = 2^L, L = 1..5 (tiny.cuh), tab_tiny.cu; nullptr
+// where no instantiation covers (L, T, exact)
+KernelFn tiny_table(int L, int T, bool exact);
 
 } // namespace ppfg

@@ -9,6 +9,7 @@
 #include "fir.cuh"
 #include "fused.cuh"
 #include "fused_split.cuh"
+#include "tiny.cuh"
 
 namespace ppfg {
 

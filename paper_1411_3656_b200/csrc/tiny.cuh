@@ -1,0 +1,132 @@
+// tiny.cuh — K6: fused FIR + C-point FFT for small power-of-two channel
+// counts (C = 2..32, SURVEY §8f row 2 "tiny C"), one warp-level kernel with
+// no HBM round trip for the filtered block and no shared memory.
+//
+// A warp holds 32 / C lane groups; lane c of a group owns channel c of a
+// contiguous time segment of output spectra. Per output spectrum the lane
+//   - slides its channel's T-spectrum window down the time axis (registers,
+//     circular by loop unrolling: every input sample is loaded once), and
+//     filters it exactly as ppf_fir_optimized (fir.hpp:85-110): FP64 FMA in
+//     ascending tap order from h0*x0 (EXACT) or an FP32 FFMA2 chain (FAST);
+//   - runs the C-point radix-2 DIT FFT ACROSS the group's lanes: stage s pairs
+//     the lanes whose labels (= channel indices, dft.hpp:106-112 bit
+//     reversal folded into the labels, fft.cuh) differ in bit L - s; both
+//     lanes of a pair get the partner's value by one shuffle and compute the
+//     same t = w * hi with the reference's operations (dft.hpp:122-131), the
+//     low lane keeping lo + t and the high lane lo - t: bit-identical to
+//     FftPlan::transform;
+//   - after the last stage lane c holds bin rev_L(c) and stores it: the group
+//     writes its C-bin row as one contiguous (permuted) segment.
+// Inputs are read through a register prefetch queue: the load of step
+// tau + min(T, 8) is issued at step tau, so that many rows per lane are in
+// flight while the window filters.
+#pragma once
+
+#include <type_traits>
+
+#include "common.cuh"
+
+namespace ppfg {
+
+template <int L, int T, bool EXACT>
+__global__ void __launch_bounds__(256) fused_tiny_kernel(const float2* __restrict__ in,
+                                                         float2* __restrict__ out, long long S_in,
+                                                         long long S_out, const float* __restrict__ taps,
+                                                         const float2* __restrict__ tw, int seg,
+                                                         long long n_tasks) {
+    constexpr int N = 1 << L;   // channels (lanes per group)
+    constexpr int G = 32 / N;   // groups (time segments) per warp
+    static_assert(L >= 1 && L <= 5, "C = 2..32");
+    using Acc = typename std::conditional<EXACT, double, float>::type;
+    const int lane = threadIdx.x & 31;
+    const int q = lane >> L;
+    const int c = lane & (N - 1);
+    const long long warp = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (warp * G >= n_tasks) // whole warp idle (uniform: shuffles need the full warp)
+        return;
+    const long long task = warp * G + q;
+    // a group past the last task runs the same (uniform) loop on row 0 and stores nothing
+    const long long s0 = task < n_tasks ? task * seg : 0;
+    const long long s1 = task < n_tasks ? min(s0 + seg, S_out) : 0;
+
+    Acc h[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t)
+        h[t] = static_cast<Acc>(__ldg(taps + t * N + c));
+    // this lane's twiddle per stage (the pair's shared tw[h-1+j], j from the
+    // label bits above the stage's bit)
+    float2 w[L];
+#pragma unroll
+    for (int s = 1; s <= L; ++s) {
+        const int b = L - s;
+        const unsigned j = s > 1 ? crev(static_cast<unsigned>(c) >> (b + 1), s - 1) : 0u;
+        w[s - 1] = __ldg(tw + (1 << (s - 1)) - 1 + j);
+    }
+    const unsigned bin = crev(static_cast<unsigned>(c), L);
+
+    auto ld = [&](long long row) {
+        row = min(row, S_in - 1);  // past the end: only feeds outputs never stored
+        return __ldcs(in + row * N + c);
+    };
+    using Win = typename std::conditional<EXACT, double2, float2>::type;
+    Win xw[T];
+#pragma unroll
+    for (int t = 0; t + 1 < T; ++t) {
+        const float2 x = ld(s0 + t);
+        xw[t].x = x.x;
+        xw[t].y = x.y;
+    }
+    // prefetch queue: the input of step tau + PF is loaded at step tau
+    constexpr int PF = T < 8 ? T : 8;
+    static_assert(T % PF == 0, "prefetch depth divides the unroll");
+    float2 nx[PF];
+#pragma unroll
+    for (int u = 0; u < PF; ++u)
+        nx[u] = ld(s0 + T - 1 + u);
+
+    for (int tau0 = 0; tau0 < seg; tau0 += T) {
+#pragma unroll
+        for (int u = 0; u < T; ++u) {
+            // newest input of this step -> circular slot (u + T - 1) % T
+            const float2 x = nx[u % PF];
+            nx[u % PF] = ld(s0 + tau0 + u + PF + T - 1);
+            xw[(u + T - 1) % T].x = x.x;
+            xw[(u + T - 1) % T].y = x.y;
+            float2 y;
+            if constexpr (EXACT) {
+                double ar = __dmul_rn(h[0], xw[u % T].x);
+                double ai = __dmul_rn(h[0], xw[u % T].y);
+#pragma unroll
+                for (int t = 1; t < T; ++t) {
+                    ar = __fma_rn(h[t], xw[(u + t) % T].x, ar);
+                    ai = __fma_rn(h[t], xw[(u + t) % T].y, ai);
+                }
+                y = make_float2(__double2float_rn(ar), __double2float_rn(ai));
+            } else {
+                y = mul2s(h[0], xw[u % T]);
+#pragma unroll
+                for (int t = 1; t < T; ++t)
+                    y = fma2s(h[t], xw[(u + t) % T], y);
+            }
+            // C-point FFT across the group's lanes (labels = lane channel c)
+#pragma unroll
+            for (int s = 1; s <= L; ++s) {
+                const int b = L - s;
+                const bool upper = (c >> b) & 1;
+                const float px = __shfl_xor_sync(0xffffffffu, y.x, 1 << b);
+                const float py = __shfl_xor_sync(0xffffffffu, y.y, 1 << b);
+                const float lx = upper ? px : y.x, ly = upper ? py : y.y;
+                const float bx = upper ? y.x : px, by = upper ? y.y : py;
+                const float tr = __fmaf_rn(bx, w[s - 1].x, -__fmul_rn(by, w[s - 1].y));
+                const float ti = __fmaf_rn(bx, w[s - 1].y, __fmul_rn(by, w[s - 1].x));
+                y = upper ? make_float2(__fsub_rn(lx, tr), __fsub_rn(ly, ti))
+                          : make_float2(__fadd_rn(lx, tr), __fadd_rn(ly, ti));
+            }
+            const long long s = s0 + tau0 + u;
+            if (s < s1)
+                __stcs(out + s * N + bin, y);
+        }
+    }
+}
+
+} // namespace ppfg

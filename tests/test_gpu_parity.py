@@ -238,6 +238,32 @@ def test_fused_vs_oracle(cuda, port, C, T, flags):
         assert err <= 1e-5 * np.log2(C), err
 
 
+@pytest.mark.parametrize("C", [2, 4, 8, 16, 32])
+@pytest.mark.parametrize("T", [1, 2, 4, 8, 16, 32])
+@pytest.mark.parametrize("mode", ["exact", "fast"])
+def test_tiny_c_fused_vs_oracle(cuda, port, C, T, mode):
+    """K6 (tiny.cuh): warp-level fused FIR + shuffle FFT for C = 2..32 —
+    EXACT bit-identical, FAST within the north-star bar; ragged segment
+    tails, a single output spectrum and a segment count that leaves idle
+    lane groups."""
+    ppf = ppf_mod()
+    coeffs = port.generate_prototype(C, T, 9.0)
+    flags = ppf.EXACT if mode == "exact" else ppf.FAST
+    for S in (T, T + 1, T + 37, 20000 + T + 3):
+        x = ppf.synth(C, S * C, seed=S + C)
+        want = port.fir_fft(x, C, T, coeffs).view(np.complex64)
+        with ppf.Plan(C, T, coeffs, flags=flags) as p:
+            got = p.fir_fft(x)
+            kind = p.kind
+        assert got.shape == (S - T + 1, C)
+        if mode == "exact":
+            assert np.array_equal(bits(got), bits(want)), (S, kind)
+        else:
+            assert max_err_over_rms(got, want) <= 1e-5 * np.log2(C), (S, kind)
+        if not (mode == "exact" and T == 32):
+            assert kind == (6 if mode == "exact" else 5)
+
+
 @pytest.mark.parametrize("S_extra", [0, 1, 2, 7, 8, 9, 100])
 def test_fused_small_and_ragged(cuda, port, S_extra):
     """n_spectra_out = 1 and tails that do not fill a batch (SURVEY §7 hard part 7)."""
