@@ -453,6 +453,8 @@ def main():
     ap.add_argument("--no-exact", action="store_true", help="skip the EXACT-mode sub-record")
     ap.add_argument("--no-parity", action="store_true", help="skip the whole-output check")
     ap.add_argument("--parity-chunk-mib", type=int, default=512)
+    ap.add_argument("--parity-all-ranks", action="store_true",
+                    help="every rank checks its own shard (default: rank 0 only)")
     ap.add_argument("--no-configs", action="store_true", help="skip the BASELINE config sweep")
     ap.add_argument("--long-gb", type=float, default=64.0,
                     help="long-stream config size on one GPU (GB of input; 0 = skip)")
@@ -468,9 +470,18 @@ def main():
 
     import torch
     import torch.distributed as dist
+    # test mode (tests/test_gpu_multirank.py): every rank on one device with
+    # gloo for the barrier / max-over-ranks, so the rank path (shards, halos,
+    # timing reduction) runs on real kernels on a one-GPU box
+    backend = os.environ.get("PPFG_BENCH_BACKEND", "nccl")
+    if os.environ.get("PPFG_BENCH_SAME_DEVICE"):
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local_rank)
     from paper_1411_3656_b200 import ppf
 
@@ -557,7 +568,21 @@ def main():
 
     # ---- parity: every output spectrum of the timed runs vs the reference ----
     parity = None
-    if rank == 0 and not args.no_parity:
+    if args.parity_all_ranks and not args.no_parity:
+        # every rank checks its own shard (halo included) and the worst one is
+        # reported: max err over ranks, mismatch counts summed
+        chunk = max(1, (args.parity_chunk_mib << 20) // (C * 8))
+        mine = full_parity(x, {args.mode: y}, C, T, coeffs.values, chunk)[args.mode]
+        parity = {args.mode: dict(mine, ranks=world,
+                                  max_err_over_rms=max_over_ranks(mine["max_err_over_rms"]),
+                                  outputs_not_bit_identical=int(sum_over_ranks(
+                                      mine["outputs_not_bit_identical"])),
+                                  n_outputs=int(sum_over_ranks(mine["n_outputs"]))),
+                  "seconds": None}
+        p = parity[args.mode]
+        p["bit_identical"] = p["outputs_not_bit_identical"] == 0
+        p["pass"] = bool(p["max_err_over_rms"] <= p["tolerance"])
+    elif rank == 0 and not args.no_parity:
         outs = {args.mode: y}
         if y_exact is not None:
             outs["exact"] = y_exact

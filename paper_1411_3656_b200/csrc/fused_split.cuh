@@ -79,8 +79,15 @@ PPFG_DEV void set_max_regs() {
 }
 
 template <int L_, int LQ_, int T_, bool EXACT_, int FIR_WG_ = 2, int W_ = 5,
-          int FIR_REGS_ = 152, int FFT_REGS_ = 104, int PC_ = 0, bool TW4_ = false>
+          int FIR_REGS_ = 152, int FFT_REGS_ = 104, int PC_ = 0, bool TW4_ = false, bool HS_ = false>
 struct SplitCfg {
+    // HS: the owner tile is handed over per FFT warpgroup (pass group pg owns
+    // rows [pg*B/2, (pg+1)*B/2)): local FULL named barrier, remote full
+    // mbarrier and the empty mbarriers all per (tile, pass group), so a pass
+    // group starts as soon as its half of the batch has landed and the FIR
+    // role refills a half as soon as its pass group has read it (fused.cuh HS)
+    static constexpr bool HS = HS_;
+    static constexpr int PG = HS_ ? 2 : 1;
     // twiddle table element: float2 (wr, wi), or pre-expanded float4 (fft.cuh tw_load)
     static constexpr bool TW4 = TW4_;
     using TwT = typename std::conditional<TW4_, float4, float2>::type;
@@ -118,18 +125,21 @@ struct SplitCfg {
     static constexpr size_t CHUNK_BYTES = sizeof(float2) * CHUNK_FLOATS2;
     static constexpr int PC = PC_ > 0 ? PC_ : int(RING_MAX / CHUNK_BYTES) < 64 ? int(RING_MAX / CHUNK_BYTES) : 64;
     static constexpr size_t RING_BYTES = CHUNK_BYTES * PC;
-    static constexpr size_t BARS = sizeof(uint64_t) * (2 * PC + 2 + 2 * Q);
+    static constexpr int PROWS = B / PG;      // tile rows per pass group
+    static constexpr int PNT = NFFT / PG;     // threads per pass group
+    static constexpr size_t BARS = sizeof(uint64_t) * (2 * PC + 2 * PG + 2 * Q * PG);
     static constexpr size_t RING_OFF = (TW_BYTES + 127) & ~size_t(127);
     static constexpr size_t TILE_OFF = RING_OFF + RING_BYTES;
     static constexpr size_t BAR_OFF = (TILE_OFF + 2 * TILE_BYTES + 7) & ~size_t(7);
-    // ring_full[PC], ring_empty[PC], full[2], empty[Q][2]
+    // ring_full[PC], ring_empty[PC], full[2][PG], empty[Q][2][PG]
     static constexpr size_t SMEM = BAR_OFF + BARS;
-    static constexpr uint32_t REMOTE_BYTES = uint32_t(sizeof(float2)) * (Q - 1) * B * (N / Q);
+    static constexpr uint32_t REMOTE_BYTES = uint32_t(sizeof(float2)) * (Q - 1) * PROWS * (N / Q); // per pass group
     // detection (POWER): as fused.cuh — last-pass units per row, per-bin
     // accumulators when the FFT role's thread count is a multiple of it
     static constexpr int UL = N >> FftSchedule<LREM, W>::width(FftSchedule<LREM, W>::NP - 1);
-    static constexpr bool POWER_OK = NFFT % UL == 0;
-    static constexpr int POWER_ROWS = NFFT / UL;
+    static constexpr bool POWER_OK = PNT % UL == 0;
+    static constexpr int POWER_ROWS = PG * (PNT / UL);
+    static_assert(!HS || B % 2 == 0, "HS splits the tile's rows over the two FFT warpgroups");
     static_assert(Q >= 2 && Q <= 8, "portable cluster sizes");
     static_assert(R >= 1 && R <= 8 && R * Q * NFIR == N, "every FIR thread owns whole channels");
     static constexpr int LAUNCH_REGS = (65536 / NT) & ~7;
@@ -160,8 +170,9 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
     float2* tiles = reinterpret_cast<float2*>(smem_raw + Cfg::TILE_OFF);
     uint64_t* ring_full = reinterpret_cast<uint64_t*>(smem_raw + Cfg::BAR_OFF);
     uint64_t* ring_empty = ring_full + PC;
-    uint64_t* full = ring_empty + PC;
-    uint64_t* empty = full + 2; // empty[d * 2 + t]
+    constexpr int PG = Cfg::PG, PROWS = Cfg::PROWS, PNT = Cfg::PNT;
+    uint64_t* full = ring_empty + PC; // full[t * PG + pg]
+    uint64_t* empty = full + 2 * PG;  // empty[(d * 2 + t) * PG + pg]
 
     const int tid = threadIdx.x;
     const uint32_t rank = cluster_rank();
@@ -180,16 +191,16 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
     if (tid < PC) {
         mbar_init(ring_full + tid, 1);
         mbar_init(ring_empty + tid, NFIR / 32);
-    } else if (tid < PC + 2) {
+    } else if (tid < PC + 2 * PG) {
         mbar_init(full + (tid - PC), 1);
-    } else if (tid < PC + 2 + 2 * Q) {
-        mbar_init(empty + (tid - PC - 2), 1);
+    } else if (tid < PC + 2 * PG + 2 * Q * PG) {
+        mbar_init(empty + (tid - PC - 2 * PG), 1);
     }
     fence_mbar_init();
     __syncthreads();
-    if (tid == NFIR) { // arm both tiles for their first fill
-        mbar_arrive_expect_tx(full + 0, Cfg::REMOTE_BYTES);
-        mbar_arrive_expect_tx(full + 1, Cfg::REMOTE_BYTES);
+    if (tid == NFIR) { // arm both tiles (every pass group's half) for their first fill
+        for (int i = 0; i < 2 * PG; ++i)
+            mbar_arrive_expect_tx(full + i, Cfg::REMOTE_BYTES);
     }
     cluster_sync_all(); // every CTA's barriers exist before anyone addresses them
 
@@ -197,6 +208,8 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
         // ================================ FFT role ================================
         set_max_regs<Cfg::FFT_REGS, Cfg::LAUNCH_REGS>();
         const int ftid = tid - NFIR;
+        const int pg = ftid / PNT;            // pass group (HS), else 0
+        const int ptid = ftid - pg * PNT;
         const TwT* tw = Cfg::TW_SMEM ? tw_s : tw_g;
         const long long n_fills = n_batches / Q;
         double pacc[POWER ? (N / Cfg::UL) : 1];
@@ -206,20 +219,21 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
         for (long long f = 0; f < n_fills; ++f) {
             const int t = static_cast<int>(f & 1);
             const long long b = f * Q + rank;
-            float2* tile = tiles + t * Cfg::TILE_FLOATS2;
+            float2* tile = tiles + t * Cfg::TILE_FLOATS2 + pg * PROWS * Cfg::STRIDE;
             if (ftid == 0) PPFG_TR(1, f, 0);
-            named_sync(1 + t, NFIR + NFFT);                          // own block written
+            named_sync(1 + t * PG + pg, NFIR + PNT);                          // own block written
             if (ftid == 0) PPFG_TR(1, f, 1);
-            mbar_wait(full + t, static_cast<uint32_t>((f >> 1) & 1)); // remote blocks landed
+            mbar_wait(full + t * PG + pg, static_cast<uint32_t>((f >> 1) & 1)); // remote blocks landed
             if (ftid == 0) PPFG_TR(1, f, 2);
-            FftPasses<Cfg::L, Cfg::LREM, Cfg::W, false, Cfg::TW_SMEM, NFFT, 0, true, POWER>::run(
-                nullptr, out, tile, Cfg::STRIDE, B, FusedRows{o0, o1, rows, b * B, B}, tw, ftid,
-                SyncNamed{5, NFFT}, pacc);
-            named_sync(5, NFFT); // every read of the tile has completed
+            FftPasses<Cfg::L, Cfg::LREM, Cfg::W, false, Cfg::TW_SMEM, PNT, 0, true, POWER>::run(
+                nullptr, out, tile, Cfg::STRIDE, PROWS,
+                OffsetRows{FusedRows{o0, o1, rows, b * B, B}, pg * PROWS}, tw, ptid,
+                SyncNamed{1 + 2 * PG + pg, PNT}, pacc);
+            named_sync(1 + 2 * PG + pg, PNT); // every read of the pass group's rows has completed
             if (ftid == 0) PPFG_TR(1, f, 3);
-            if (ftid == 0) {
-                mbar_arrive_expect_tx(full + t, Cfg::REMOTE_BYTES); // arm the next fill
-                const uint32_t e = smem_u32(empty + rank * 2 + t);
+            if (ptid == 0) {
+                mbar_arrive_expect_tx(full + t * PG + pg, Cfg::REMOTE_BYTES); // arm the next fill
+                const uint32_t e = smem_u32(empty + (rank * 2 + t) * PG + pg);
 #pragma unroll
                 for (int q = 0; q < Q; ++q)
                     mbar_arrive_remote_relaxed(mapa(e, static_cast<uint32_t>(q)));
@@ -228,8 +242,8 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
         if constexpr (POWER) {
             static_assert(Cfg::POWER_OK, "per-bin accumulators");
             constexpr int UL = Cfg::UL, EL = N / UL;
-            const int r = ftid / UL;
-            const unsigned u = static_cast<unsigned>(ftid % UL);
+            const int r = pg * (PNT / UL) + ptid / UL;
+            const unsigned u = static_cast<unsigned>(ptid % UL);
             double* part = reinterpret_cast<double*>(out) +
                            (static_cast<size_t>(blockIdx.x) * Cfg::POWER_ROWS + r) * N + u;
 #pragma unroll
@@ -307,13 +321,13 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
             const int d = static_cast<int>(b - f * Q); // owner CTA
             const int t = static_cast<int>(f & 1);     // owner's tile
             if (tid == 0) PPFG_TR(0, b, 0);
-            if (f >= 2)
+            if (!Cfg::HS && f >= 2)
                 mbar_wait(empty + d * 2 + t, static_cast<uint32_t>(((f >> 1) - 1) & 1));
             if (tid == 0) PPFG_TR(0, b, 1);
             const bool local = (static_cast<uint32_t>(d) == rank);
             const uint32_t tile_u32 = tiles_u32 + static_cast<uint32_t>(t * Cfg::TILE_BYTES);
             const uint32_t rtile = mapa(tile_u32, static_cast<uint32_t>(d));
-            const uint32_t rbar = mapa(full_u32 + t * 8u, static_cast<uint32_t>(d));
+            const uint32_t rbar0 = mapa(full_u32 + t * PG * 8u, static_cast<uint32_t>(d));
             constexpr int CPB = B / Cfg::RB;       // chunks per batch
             const long long c0 = b * CPB;         // this batch's chunks c0 .. c0+CPB-1
             if (producer) {
@@ -351,6 +365,12 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
             if (tid == 0) PPFG_TR(0, b, 2);
 #pragma unroll
             for (int i = 0; i < B; ++i) {
+                if constexpr (Cfg::HS) { // the owner's pass group i / PROWS has read tile t
+                    if (i % PROWS == 0 && f >= 2)
+                        mbar_wait(empty + (d * 2 + t) * PG + i / PROWS,
+                                  static_cast<uint32_t>(((f >> 1) - 1) & 1));
+                }
+                const uint32_t rbar = rbar0 + 8u * static_cast<uint32_t>(i / PROWS);
                 const float2* chunk = ring + slot[i / Cfg::RB] * Cfg::CHUNK_FLOATS2 +
                                       (i % Cfg::RB) * (R * RUN) + j;
                 float2 y[R];
@@ -385,6 +405,10 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
                     const uint32_t off = 8u * (i * Cfg::STRIDE + slot_of[k]);
                     st_local_or_async_f2(local, ltile_u32 + off, rtile + off, y[k], rbar);
                 }
+                if constexpr (Cfg::HS) { // own block of pass group i / PROWS written
+                    if (local && (i + 1) % PROWS == 0)
+                        named_arrive(1 + t * PG + i / PROWS, NFIR + PNT);
+                }
             }
             if (tid == 0) PPFG_TR(0, b, 3);
             __syncwarp();
@@ -394,7 +418,7 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
                     if (c0 + i < n_chunks)
                         mbar_arrive_relaxed(ring_empty + slot[i]);
             }
-            if (local)
+            if (!Cfg::HS && local)
                 named_arrive(1 + t, NFIR + NFFT); // own block of tile t written
         }
     }

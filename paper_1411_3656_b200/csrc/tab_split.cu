@@ -4,6 +4,11 @@
 namespace ppfg {
 
 std::vector<FusedEntry> fused_part_split() {
+    // Round 2: per-pass-group owner-tile handoff (SplitCfg HS, the 11th
+    // argument) where it measured faster (1 GiB): C=1024 T=16 0.645 -> 0.70,
+    // EXACT C=1024 T=8 0.63 -> 0.645 (6.5 GB SKA EXACT 0.668 -> 0.682), EXACT
+    // T=16 0.403 -> 0.411, C=2048 0.69 -> 0.71, C=4096 0.533 -> 0.537, T=32
+    // 0.416 -> 0.420; not EXACT C=2048 (0.474 -> 0.463).
     return {
         // thread-block clusters, FIR split by channel block and FFT by
         // spectrum (fused_split.cuh) — for FIR state that does not fit one SM.
@@ -24,13 +29,13 @@ std::vector<FusedEntry> fused_part_split() {
         // 0.53; FP64 T=16 168/88 0.402 vs 0.403; FAST T=32 cluster 136/120
         // 0.41, 168/88 0.42, 8-CTA 0.28 — all below unfused K1b 0.43)
 
-        split_entry<SplitCfg<10, 1, 16, false, 2, 5, 136, 120, 0, true>>(true),
-        split_entry<SplitCfg<10, 2, 32, false, 2, 5, 152, 104, 0, true>>(false),
-        split_entry<SplitCfg<10, 1, 8, true, 2, 5, 136, 120, 0, true>>(true),
-        split_entry<SplitCfg<10, 2, 16, true, 2, 5, 152, 104, 0, true>>(true),
-        split_entry<SplitCfg<11, 1, 8, false, 2, 5, 136, 120>>(true),
+        split_entry<SplitCfg<10, 1, 16, false, 2, 5, 136, 120, 0, true, true>>(true),
+        split_entry<SplitCfg<10, 2, 32, false, 2, 5, 152, 104, 0, true, true>>(false),
+        split_entry<SplitCfg<10, 1, 8, true, 2, 5, 136, 120, 0, true, true>>(true),
+        split_entry<SplitCfg<10, 2, 16, true, 2, 5, 152, 104, 0, true, true>>(true),
+        split_entry<SplitCfg<11, 1, 8, false, 2, 5, 136, 120, 0, false, true>>(true),
         split_entry<SplitCfg<11, 2, 8, true, 2, 5, 152, 104, 0, true>>(true),
-        split_entry<SplitCfg<12, 2, 8, false>>(true),
+        split_entry<SplitCfg<12, 2, 8, false, 2, 5, 152, 104, 0, false, true>>(true),
         split_entry<SplitCfg<13, 3, 8, false>>(false),
     };
 }
