@@ -124,11 +124,11 @@ struct FftSchedule {
 // accumulators pacc[k] — the caller guarantees one unit per thread, so
 // pacc[k] always belongs to the same tile row and bin.
 template <int L, int LO, int W, bool FIRST_GLOBAL, bool FINAL, bool TW_SMEM, int NT, bool POWER = false,
-          class RowMap, class TW>
+          class RowMap, class TW, class PA = double>
 PPFG_DEV void fft_tile_pass(const float2* gin, float2* gout,
                             float2* __restrict__ tile, unsigned row_stride, int rows,
                             const RowMap& map, const TW* __restrict__ tw, int tid,
-                            double* pacc = nullptr) {
+                            PA* pacc = nullptr) {
     constexpr int N = 1 << L;
     constexpr int E = 1 << W;
     constexpr int HI = LO + W - 1;
@@ -167,9 +167,13 @@ PPFG_DEV void fft_tile_pass(const float2* gin, float2* gout,
         if constexpr (FINAL && POWER) {
             if (map(r) >= 0) {
 #pragma unroll
-                for (int k = 0; k < E; ++k)
-                    pacc[k] += static_cast<double>(v[k].x) * v[k].x +
-                               static_cast<double>(v[k].y) * v[k].y;
+                for (int k = 0; k < E; ++k) {
+                    if constexpr (sizeof(PA) == 8)
+                        pacc[k] += static_cast<double>(v[k].x) * v[k].x +
+                                   static_cast<double>(v[k].y) * v[k].y;
+                    else // FAST detection: FP32 partial sums, flushed to FP64 by the caller
+                        pacc[k] = __fmaf_rn(v[k].x, v[k].x, __fmaf_rn(v[k].y, v[k].y, pacc[k]));
+                }
             }
         } else if constexpr (FINAL) {
             const long long grow = map(r);
@@ -205,10 +209,10 @@ struct FftPasses {
     static constexpr int LO = S::lo(I);
     static constexpr bool LAST = (I == S::NP - 1);
     static constexpr int E_LAST = 1 << S::width(S::NP - 1); // values per unit in the last pass
-    template <class RowMap, class Sync, class TW>
+    template <class RowMap, class Sync, class TW, class PA = double>
     PPFG_DEV static void run(const float2* gin, float2* gout, float2* tile, unsigned row_stride,
                              int rows, const RowMap& map, const TW* tw, int tid,
-                             const Sync& sync, double* pacc = nullptr) {
+                             const Sync& sync, PA* pacc = nullptr) {
         fft_tile_pass<L, LO, WI, FIRST_GLOBAL && I == 0, LAST && STORE_LAST, TW_SMEM, NT,
                       LAST && POWER>(gin, gout, tile, row_stride, rows, map, tw, tid, pacc);
         if constexpr (!LAST) {

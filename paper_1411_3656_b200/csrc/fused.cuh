@@ -228,10 +228,37 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
         const int ptid = ftid - pg * PNT;
         using Passes = FftPasses<L, L - RLOG, Cfg::W, false, true, PNT, 0, true, POWER>;
         constexpr int EL = Passes::E_LAST;
-        double pacc[POWER ? EL : 1];
+        // detection accumulators: FP64 in EXACT mode (cmd_inspect's double
+        // running sum up to order); FP32 in FAST mode, flushed into the CTA's
+        // FP64 partial row every kFlush batches (fewer registers, no FP64 /
+        // conversion work per bin; adds <= kFlush FP32 roundings per partial)
+        using PA = typename std::conditional<Cfg::EXACT, double, float>::type;
+        constexpr long long kFlush = 16;
+        PA pacc[POWER ? EL : 1];
 #pragma unroll
         for (int k = 0; k < (POWER ? EL : 1); ++k)
-            pacc[k] = 0.0;
+            pacc[k] = 0;
+        double* part = nullptr;
+        if constexpr (POWER) {
+            // every last-pass unit of this thread (tile rows ptid / UL +
+            // m * PNT / UL) covers bins u + rev_L(k): partial row r of the CTA
+            constexpr int UL = N / EL;
+            static_assert(UL == Cfg::UL && Cfg::POWER_OK, "per-bin accumulators");
+            const int r = pg * (PNT / UL) + ptid / UL;
+            const unsigned u = static_cast<unsigned>(ptid % UL);
+            part = reinterpret_cast<double*>(out) +
+                   (static_cast<size_t>(blockIdx.x) * Cfg::POWER_ROWS + r) * N + u;
+        }
+        bool flushed = false; // the partial row holds a value (else: store, not add)
+        auto flush = [&]() {
+#pragma unroll
+            for (int k = 0; k < EL; ++k) {
+                double* d = part + crev(static_cast<unsigned>(k), L);
+                *d = (flushed ? *d : 0.0) + static_cast<double>(pacc[k]);
+                pacc[k] = 0;
+            }
+            flushed = true;
+        };
         const int hpg = Cfg::HS ? pg : 0;
         for (long long b = 0; b < n_batches; ++b) {
             const int t = static_cast<int>(b % Cfg::NTILE);
@@ -241,20 +268,13 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
                         PROWS, OffsetRows{FusedRows{o0, o1, rpg, b * B, B}, pg * PROWS}, tw, ptid,
                         SyncNamed{Cfg::bar_pass(pg), PNT}, pacc);
             named_arrive(Cfg::bar_empty(t, hpg), Cfg::hcount(hpg));
+            if constexpr (POWER && !Cfg::EXACT) {
+                if ((b + 1) % kFlush == 0)
+                    flush();
+            }
         }
-        if constexpr (POWER) {
-            // every last-pass unit of this thread (tile rows ptid / UL +
-            // m * PNT / UL) covers bins u + rev_L(k): partial row r of the CTA
-            constexpr int UL = N / EL;
-            static_assert(UL == Cfg::UL && Cfg::POWER_OK, "per-bin accumulators");
-            const int r = pg * (PNT / UL) + ptid / UL;
-            const unsigned u = static_cast<unsigned>(ptid % UL);
-            double* part = reinterpret_cast<double*>(out) +
-                           (static_cast<size_t>(blockIdx.x) * Cfg::POWER_ROWS + r) * N + u;
-#pragma unroll
-            for (int k = 0; k < EL; ++k)
-                part[crev(static_cast<unsigned>(k), L)] = pacc[k];
-        }
+        if constexpr (POWER)
+            flush();
         return;
     }
 

@@ -212,10 +212,34 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
         const int ptid = ftid - pg * PNT;
         const TwT* tw = Cfg::TW_SMEM ? tw_s : tw_g;
         const long long n_fills = n_batches / Q;
-        double pacc[POWER ? (N / Cfg::UL) : 1];
+        // detection accumulators (as fused.cuh): FP64 in EXACT mode, FP32 in
+        // FAST mode flushed into the CTA's FP64 partial row every kFlush fills
+        using PA = typename std::conditional<Cfg::EXACT, double, float>::type;
+        constexpr long long kFlush = 16;
+        constexpr int EL = POWER ? N / Cfg::UL : 1;
+        PA pacc[EL];
 #pragma unroll
-        for (int k = 0; k < (POWER ? N / Cfg::UL : 1); ++k)
-            pacc[k] = 0.0;
+        for (int k = 0; k < EL; ++k)
+            pacc[k] = 0;
+        double* part = nullptr;
+        if constexpr (POWER) {
+            static_assert(Cfg::POWER_OK, "per-bin accumulators");
+            constexpr int UL = Cfg::UL;
+            const int r = pg * (PNT / UL) + ptid / UL;
+            const unsigned u = static_cast<unsigned>(ptid % UL);
+            part = reinterpret_cast<double*>(out) +
+                   (static_cast<size_t>(blockIdx.x) * Cfg::POWER_ROWS + r) * N + u;
+        }
+        bool flushed = false;
+        auto flush = [&]() {
+#pragma unroll
+            for (int k = 0; k < EL; ++k) {
+                double* d = part + crev(static_cast<unsigned>(k), Cfg::L);
+                *d = (flushed ? *d : 0.0) + static_cast<double>(pacc[k]);
+                pacc[k] = 0;
+            }
+            flushed = true;
+        };
         for (long long f = 0; f < n_fills; ++f) {
             const int t = static_cast<int>(f & 1);
             const long long b = f * Q + rank;
@@ -238,18 +262,13 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
                 for (int q = 0; q < Q; ++q)
                     mbar_arrive_remote_relaxed(mapa(e, static_cast<uint32_t>(q)));
             }
+            if constexpr (POWER && !Cfg::EXACT) {
+                if ((f + 1) % kFlush == 0)
+                    flush();
+            }
         }
-        if constexpr (POWER) {
-            static_assert(Cfg::POWER_OK, "per-bin accumulators");
-            constexpr int UL = Cfg::UL, EL = N / UL;
-            const int r = pg * (PNT / UL) + ptid / UL;
-            const unsigned u = static_cast<unsigned>(ptid % UL);
-            double* part = reinterpret_cast<double*>(out) +
-                           (static_cast<size_t>(blockIdx.x) * Cfg::POWER_ROWS + r) * N + u;
-#pragma unroll
-            for (int k = 0; k < EL; ++k)
-                part[crev(static_cast<unsigned>(k), Cfg::L)] = pacc[k];
-        }
+        if constexpr (POWER)
+            flush();
         cluster_sync_all();
         return;
     }

@@ -497,7 +497,9 @@ def test_fir_fft_mean_power(cuda, port, C, T, flags):
         bins = p.fir_fft(x)
         via_bins = p.mean_power(bins)
     want = port.mean_power(port.fir_fft(x, C, T, coeffs), C)
-    assert _rel(fused, via_bins) <= 1e-13
+    # EXACT: FP64 accumulation, only the summation order differs; FAST: FP32
+    # partial sums of 16 batches flushed into FP64 partials (fused.cuh)
+    assert _rel(fused, via_bins) <= (1e-13 if flags == "exact" else 5e-6)
     if flags == "exact":
         assert _rel(fused, want) <= 1e-13              # bins bit-exact: only the sum order differs
     else:
