@@ -673,7 +673,7 @@ def main():
             "x_realtime": value * 1e9 / SKA_RATE,
             "config": {"workload": desc, "n_channels": C, "n_taps": T,
                        "n_spectra_in_per_gpu": ic, "bytes_in_per_gpu": bytes_in,
-                       "mode": args.mode, "kernel": ["unfused", "fused-fp32", "fused-fp64", "cluster-fp32", "cluster-fp64", "tiny-fp32", "tiny-fp64"][kind],
+                       "mode": args.mode, "kernel": ["unfused", "fused-fp32", "fused-fp64", "cluster-fp32", "cluster-fp64", "tiny-fp32", "tiny-fp64", "l2x-fp32", "l2x-fp64"][kind],
                        "l2": "inputs >> 126 MB L2 (no flush needed)", "parallelism": f"shard{world}"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,

@@ -69,8 +69,10 @@ enum {
     PPFG_CLUSTER = 4u,
     PPFG_K1_PREFETCH = 8u, /* comparison only: FIR-only kernel with register prefetch
                               instead of TMA-staged input (same results) */
-    PPFG_FIR_LEGACY = 16u  /* comparison only: the lane-window FIR kernels (K1/K1t/K1f)
+    PPFG_FIR_LEGACY = 16u, /* comparison only: the lane-window FIR kernels (K1/K1t/K1f)
                               instead of the register-blocked K1b for T >= 16 */
+    PPFG_L2X = 32u         /* also admit the L2-exchange fused kernels (K7, l2x.cuh)
+                              that are not taken by default */
 };
 
 typedef struct ppfg_plan_s* ppfg_plan;
@@ -148,7 +150,8 @@ int ppfg_fir_fft_mean_power(ppfg_plan plan, const void* in, uint64_t n_spectra_i
 
 /* Which kernel ppfg_fir_fft will run for this plan: 0 = unfused FIR+FFT,
  * 1 = fused FP32-FIR, 2 = fused FP64 (bit-exact) FIR, 3 / 4 = the cluster
- * versions of 1 / 2, 5 / 6 = the warp-level tiny-C (2..32) versions of 1 / 2. */
+ * versions of 1 / 2, 5 / 6 = the warp-level tiny-C (2..32) versions of 1 / 2,
+ * 7 / 8 = the L2-exchange versions (K7) of 1 / 2. */
 int ppfg_fir_fft_kind(ppfg_plan plan);
 /* The kernel ppfg_fir_fft launches for this plan, named the way ncu prints it
  * ("fused_fir_fft_kernel<FusedCfg<10, 8, 2, 0, ...>>"), so measurements can be

@@ -155,8 +155,8 @@ PPFG_DEV void fft_tile_pass(const float2* gin, float2* gout,
             const long long grow = map(r);
             const float2* src = gin + grow * N + fixed;
 #pragma unroll
-            for (int k = 0; k < E; ++k)
-                v[k] = grow >= 0 ? src[static_cast<unsigned>(k) << LO] : make_float2(0.f, 0.f);
+            for (int k = 0; k < E; ++k) // L2-only loads: the rows may have been written by other SMs
+                v[k] = grow >= 0 ? __ldcg(src + (static_cast<unsigned>(k) << LO)) : make_float2(0.f, 0.f);
         } else {
             const float2* src = tile + r * row_stride + sw(fixed);
 #pragma unroll

@@ -1,0 +1,295 @@
+// l2x.cuh — K7: fused FIR + C-point FFT through an L2-resident exchange ring,
+// for the shapes whose FIR state does not fit the SMs' registers next to the
+// FFT (long filters, T = 32 / 64 at C = 1024; very long transforms,
+// C = 8192): one persistent kernel, one CTA per SM, two warp-specialised roles
+// that exchange the filtered spectra through a small ring buffer in global
+// memory sized to stay in the 126 MB L2, instead of through the HBM round trip
+// of FIR -> HBM -> FFT (pipeline.hpp:125-127) or through DSMEM (K3s).
+//
+//  FIR role (NWF warps): work item (k, cb) = output spectra [k*CS, (k+1)*CS)
+//    of channels [32*cb, 32*cb + 32), items k-major, item i on CTA i mod grid.
+//    Its input (CS + T - 1 spectra x 32 channels) streams through a TMA ring of
+//    2-D tensor copies (box {32 channels, RB rows}, SASS UTMALDG); each warp
+//    computes U consecutive outputs of its lane's channel per step, reading
+//    every input row once from shared memory and applying it to all U
+//    accumulators (register blocking over time, as K1b in fir.cuh: taps in
+//    registers, each output accumulated in ascending tap order — FP64 from
+//    h0*x0 in EXACT mode, bit-identical to ppf_fir_optimized, fir.hpp:85-110;
+//    FP32 FFMA2 in FAST mode). The outputs go to ring slot k mod NSR (plain
+//    stores, L2), then the item is published: __threadfence by every thread,
+//    a role barrier, one release add on produced[slot].
+//  FFT role (NFFT warps): tile (k, i) = BT consecutive spectra of chunk k, tile
+//    j on CTA j mod grid. Its leader waits (acquire spin) until all C/32 items
+//    of chunk k are published, the first pass loads the rows from the ring
+//    with L2-only loads (ld.global.cg: the L1 may hold a stale copy of an
+//    earlier use of the slot), the remaining radix-2 passes run through a
+//    shared-memory tile (fft.cuh: the reference's butterflies and twiddles,
+//    bit-identical to FftPlan::transform, dft.hpp:100-148) and the last pass
+//    stores natural-order bins to HBM; after the first pass the leader adds
+//    the tile's rows to consumed[slot].
+//  Back-pressure: a FIR item writes slot k mod NSR only when every row of
+//    chunk k - NSR has been consumed. Every wait is on an earlier chunk than
+//    the waiter's own, and all CTAs are co-resident (grid <= SMs, one CTA
+//    each), so the pipeline cannot deadlock.
+// The ring is NSR * CS * C * 8 bytes (16 MB at C = 1024), written and read
+// while it is resident in L2, so the filtered block costs L2 traffic, not HBM
+// traffic (checked with ncu: dram bytes vs the algorithmic 8*C*(S_in+S_out)).
+#pragma once
+
+#include <cuda.h>
+
+#include <type_traits>
+
+#include "fused.cuh"
+
+namespace ppfg {
+
+template <int L_, int T_, bool EXACT_, int U_ = 16, int NWF_ = 4, int CSR_ = 4, int NS_ = 6,
+          int NSR_ = 8, int NWT_ = 8, int W_ = 5, int FIR_REGS_ = 168, int FFT_REGS_ = 128>
+struct L2xCfg {
+    static constexpr int L = L_, T = T_, N = 1 << L;
+    static constexpr bool EXACT = EXACT_;
+    static constexpr int U = U_, NWF = NWF_, NFIR = 32 * NWF_;
+    static constexpr int RB = NWF_ * U_;          // input rows per TMA chunk = outputs per step
+    static constexpr int CSR = CSR_;              // steps per work item
+    static constexpr int CS = CSR_ * RB;          // output spectra per chunk (work item)
+    static constexpr int NS = NS_;                // input ring chunks
+    static constexpr int NSR = NSR_;              // L2 ring slots (chunks of CS spectra)
+    static constexpr int NCB = N / 32;            // channel blocks = items per chunk
+    static constexpr int NIC = (CS + T - 1 + RB - 1) / RB;  // input chunks per item
+    static constexpr int NEED = 1 + (T - 1 + RB - 1) / RB;  // input chunks one step reads
+    static constexpr int NFFT = 32 * NWT_, NT = NFIR + NFFT;
+    static constexpr int W = W_;
+    static constexpr int WMAX = FftSchedule<L, W>::width(0);
+    static constexpr int BT = (NFFT << WMAX) / N > 0 ? (NFFT << WMAX) / N : 1; // spectra per FFT tile
+    static constexpr int TPC = CS / BT;           // FFT tiles per chunk
+    static constexpr int FIR_REGS = FIR_REGS_, FFT_REGS = FFT_REGS_;
+    static constexpr unsigned STRIDE = sw_row_stride(N);
+    static constexpr size_t CHUNK_BYTES = sizeof(float2) * RB * 32;
+    static constexpr size_t TW_BYTES = sizeof(float2) * N;
+    static constexpr size_t RING_OFF = (TW_BYTES + 127) & ~size_t(127);
+    static constexpr size_t TILE_OFF = RING_OFF + CHUNK_BYTES * NS;
+    static constexpr size_t TILE_BYTES = sizeof(float2) * size_t(BT) * STRIDE;
+    static constexpr size_t BAR_OFF = (TILE_OFF + TILE_BYTES + 7) & ~size_t(7);
+    static constexpr size_t SMEM = BAR_OFF + sizeof(uint64_t) * NS;
+    static constexpr size_t RING_SLOT_FLOATS2 = size_t(CS) * N; // one L2 ring slot
+    static constexpr int LAUNCH_REGS = (65536 / NT) & ~7;
+    static_assert(N >= 32 && CS % BT == 0, "whole FFT tiles per chunk");
+    static_assert(NS >= NEED + 1, "input ring: a step's chunks plus lookahead");
+    static_assert((RB & (RB - 1)) == 0 && RB <= 256, "power-of-two chunks within a TMA box");
+    static_assert(FIR_REGS * NFIR + FFT_REGS * NFFT <= LAUNCH_REGS * NT, "register split");
+    static_assert(SMEM <= 232448, "shared memory per CTA");
+};
+
+// device-scope acquire load / release add of the ring counters
+PPFG_DEV unsigned ld_acquire_gpu(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+PPFG_DEV void red_release_gpu_add(unsigned* p, unsigned v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+PPFG_DEV void spin_until_geq(const unsigned* p, unsigned target) {
+    if (ld_acquire_gpu(p) >= target)
+        return;
+    unsigned ns = 32;
+    while (ld_acquire_gpu(p) < target) {
+        __nanosleep(ns);
+        ns = ns < 256 ? ns * 2 : ns;
+    }
+}
+
+// Output rows of an FFT tile: spectra row0 .. row0 + BT - 1 (k*CS + i*BT),
+// -1 past the end. The ring is addressed through the same row index: the
+// caller shifts the ring pointer by -row_of_slot so gin + row * N lands in
+// the slot.
+struct L2xRows {
+    long long row0, n_rows;
+    PPFG_DEV long long operator()(int r) const { return row0 + r < n_rows ? row0 + r : -1; }
+};
+
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::NT, 1)
+    fused_l2x_kernel(const __grid_constant__ CUtensorMap in_map, float2* __restrict__ out,
+                     float2* __restrict__ ring, unsigned* __restrict__ ctr, long long S_out,
+                     const float* __restrict__ taps, const float2* __restrict__ tw_g) {
+    constexpr int L = Cfg::L, T = Cfg::T, N = Cfg::N, U = Cfg::U, RB = Cfg::RB, CS = Cfg::CS;
+    constexpr int NS = Cfg::NS, NSR = Cfg::NSR, NCB = Cfg::NCB, NIC = Cfg::NIC, NEED = Cfg::NEED;
+    constexpr int NFIR = Cfg::NFIR, NFFT = Cfg::NFFT, BT = Cfg::BT, TPC = Cfg::TPC;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    float2* tw = reinterpret_cast<float2*>(smem_raw);
+    float2* in_ring = reinterpret_cast<float2*>(smem_raw + Cfg::RING_OFF);
+    float2* tile = reinterpret_cast<float2*>(smem_raw + Cfg::TILE_OFF);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + Cfg::BAR_OFF);
+    unsigned* produced = ctr;        // [NSR]: items published per slot (all epochs)
+    unsigned* consumed = ctr + NSR;  // [NSR]: rows read per slot (all epochs)
+
+    const int tid = threadIdx.x;
+    const long long n_chunks = (S_out + CS - 1) / CS;
+    const long long grid = gridDim.x;
+
+    for (int i = tid; i < N - 1; i += Cfg::NT)
+        tw[i] = tw_g[i];
+    if (tid < NS)
+        mbar_init(full + tid, 1);
+    fence_mbar_init();
+    __syncthreads();
+
+    if (tid >= NFIR) {
+        // ================================ FFT role ================================
+        if constexpr (Cfg::FFT_REGS < Cfg::LAUNCH_REGS)
+            asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(Cfg::FFT_REGS));
+        const int ftid = tid - NFIR;
+        constexpr int BAR_FFT = 2; // named barrier of the FFT warps
+        const long long n_tiles = n_chunks * TPC;
+        for (long long j = blockIdx.x; j < n_tiles; j += grid) {
+            const long long k = j / TPC;
+            const int slot = static_cast<int>(k % NSR);
+            const unsigned epoch = static_cast<unsigned>(k / NSR);
+            if (ftid == 0)
+                spin_until_geq(produced + slot, (epoch + 1) * NCB); // chunk k published
+            named_sync(BAR_FFT, NFFT);
+            const long long row0 = k * CS + (j - k * TPC) * BT;
+            // ring row (slot, r) == gin + (k*CS + r) * N
+            const float2* gin = ring + slot * Cfg::RING_SLOT_FLOATS2 - k * CS * static_cast<long long>(N);
+            FftPasses<L, L, Cfg::W, true, true, NFFT>::run(gin, out, tile, Cfg::STRIDE, BT,
+                                                          L2xRows{row0, S_out}, tw, ftid,
+                                                          SyncNamed{BAR_FFT, NFFT});
+            // every thread's ring loads completed in the first pass (before
+            // its barrier); release the tile's rows and the smem tile
+            named_sync(BAR_FFT, NFFT);
+            if (ftid == 0)
+                red_release_gpu_add(consumed + slot, BT);
+        }
+        return;
+    }
+
+    // ================================== FIR role ==================================
+    if constexpr (Cfg::FIR_REGS > Cfg::LAUNCH_REGS)
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(Cfg::FIR_REGS));
+    constexpr int BAR_FIR = 1;
+    const int warp = tid >> 5, lane = tid & 31;
+    const long long n_items = n_chunks * NCB;
+    // this CTA's items: blockIdx.x + m * grid; its input chunks form one
+    // sequence g = m * NIC + q (item m, chunk q of the item)
+    const long long my_items = n_items > blockIdx.x ? (n_items - blockIdx.x + grid - 1) / grid : 0;
+    const long long my_chunks = my_items * NIC;
+    auto issue = [&](long long g) { // FIR thread 0 only
+        const long long m = g / NIC;
+        const int q = static_cast<int>(g - m * NIC);
+        const long long item = blockIdx.x + m * grid;
+        const long long k = item / NCB;
+        const int cb = static_cast<int>(item - k * NCB);
+        const int s = static_cast<int>(g % NS);
+        mbar_arrive_expect_tx(full + s, static_cast<uint32_t>(Cfg::CHUNK_BYTES));
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(in_ring + s * RB * 32)),
+            "l"(reinterpret_cast<uint64_t>(&in_map)), "r"(cb * 32),
+            "r"(static_cast<int>(k * CS + q * RB)), "r"(smem_u32(full + s))
+            : "memory");
+    };
+    long long issued = 0;
+    if (tid == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&in_map)) : "memory");
+        for (; issued < NS && issued < my_chunks; ++issued)
+            issue(issued);
+    }
+    using acc_t = typename std::conditional<Cfg::EXACT, double2, float2>::type;
+    using tap_t = typename std::conditional<Cfg::EXACT, double, float>::type;
+    long long waited = 0; // input chunks whose arrival this thread has waited for
+    int cb_prev = -1;
+    tap_t h[T];
+    for (long long m = 0; m < my_items; ++m) {
+        const long long item = blockIdx.x + m * grid;
+        const long long k = item / NCB;
+        const int cb = static_cast<int>(item - k * NCB);
+        const int slot = static_cast<int>(k % NSR);
+        if (cb != cb_prev) { // taps of this lane's channel
+#pragma unroll
+            for (int t = 0; t < T; ++t)
+                h[t] = static_cast<tap_t>(__ldg(taps + static_cast<size_t>(t) * N + cb * 32 + lane));
+            cb_prev = cb;
+        }
+        // the slot's previous chunk (k - NSR) has been read by every FFT tile
+        if (tid == 0)
+            spin_until_geq(consumed + slot, static_cast<unsigned>(k / NSR) * CS);
+        named_sync(BAR_FIR, NFIR);
+        float2* dst = ring + slot * Cfg::RING_SLOT_FLOATS2 + cb * 32 + lane;
+        const long long g0 = m * NIC; // this item's first input chunk
+#pragma unroll 1
+        for (int st = 0; st < Cfg::CSR; ++st) {
+            if (st > 0) {
+                // every FIR warp is done with step st-1, the last reader of chunk g0+st-1
+                named_sync(BAR_FIR, NFIR);
+                if (tid == 0)
+                    for (; issued < my_chunks && issued < g0 + st + NS; ++issued) // chunk g reuses the slot of g - NS
+                        issue(issued);
+            }
+            const long long need = min(g0 + st + NEED - 1, g0 + NIC - 1);
+            for (; waited <= need; ++waited)
+                mbar_wait(full + static_cast<int>(waited % NS), static_cast<uint32_t>((waited / NS) & 1));
+            // rows st*RB + warp*U + [0, U + T - 1) of the item's input
+            const int r0 = st * RB + warp * U;
+            acc_t acc[U];
+            const uint32_t ring_u32 = smem_u32(in_ring) + 8u * static_cast<uint32_t>(lane);
+            const int s0 = static_cast<int>((g0 + st) % NS); // ring slot of the step's first chunk
+            const int wb = warp * U;                           // the warp's first row in the step
+#pragma unroll
+            for (int jj = 0; jj < U + T - 1; ++jj) {
+                // item-relative row st*RB + wb + jj: chunk st + q, row o of it
+                const int q = (wb + jj) / RB, o = (wb + jj) & (RB - 1);
+                const int s = s0 + q >= NS ? s0 + q - NS : s0 + q;
+                // volatile: keeps each row's load next to its FMAs (hoisting
+                // all U + T - 1 loads ahead would spill)
+                float2 x;
+                asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];"
+                             : "=f"(x.x), "=f"(x.y)
+                             : "r"(ring_u32 + 256u * static_cast<uint32_t>(s * RB + o)));
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int t = jj - u;
+                    if (t < 0 || t >= T)
+                        continue;
+                    if constexpr (Cfg::EXACT) {
+                        const double xr = static_cast<double>(x.x), xi = static_cast<double>(x.y);
+                        if (t == 0) {
+                            acc[u].x = __dmul_rn(h[0], xr);
+                            acc[u].y = __dmul_rn(h[0], xi);
+                        } else {
+                            acc[u].x = __fma_rn(h[t], xr, acc[u].x);
+                            acc[u].y = __fma_rn(h[t], xi, acc[u].y);
+                        }
+                    } else {
+                        if (t == 0)
+                            acc[u] = mul2s(h[0], x);
+                        else
+                            acc[u] = fma2s(h[t], x, acc[u]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                float2 y;
+                if constexpr (Cfg::EXACT)
+                    y = make_float2(__double2float_rn(acc[u].x), __double2float_rn(acc[u].y));
+                else
+                    y = acc[u];
+                dst[static_cast<size_t>(r0 + u) * N] = y;
+            }
+        }
+        // publish the item: every thread's ring stores are visible at GPU
+        // scope before the release add
+        __threadfence();
+        named_sync(BAR_FIR, NFIR);
+        if (tid == 0) {
+            red_release_gpu_add(produced + slot, 1);
+            // the item's remaining input chunks are released: refill
+            for (; issued < my_chunks && issued < g0 + NIC + NS; ++issued)
+                issue(issued);
+        }
+    }
+}
+
+} // namespace ppfg

@@ -90,6 +90,11 @@ struct DeviceGuard {
 
 // -------------------------------------------------------- kernel tables
 // (tables.h; the kernel instantiations are compiled in the tab_*.cu units)
+const std::vector<L2xEntry>& l2x_entries() {
+    static const std::vector<L2xEntry> t = l2x_table();
+    return t;
+}
+
 const std::vector<FusedEntry>& fused_table() {
     static const std::vector<FusedEntry> t = [] {
         std::vector<FusedEntry> v;
@@ -211,6 +216,12 @@ struct ppfg_plan_s {
     bool own_stream = false;
     const FusedEntry* fused = nullptr;
     std::string fused_name; // the fused kernel's configuration, as ncu prints it
+    // K7 (l2x.cuh): the exchange ring + its counters (grow-only) and an event
+    // ordering launches that share them
+    const L2xEntry* l2x = nullptr;
+    void* d_ring = nullptr;
+    size_t ring_bytes = 0;
+    cudaEvent_t ev_ring = nullptr;
     // host-mode pipeline buffers (grow-only)
     void* d_in[2] = {nullptr, nullptr};
     void* d_out[2] = {nullptr, nullptr};
@@ -697,7 +708,42 @@ bool launch_tiny(ppfg_plan p, const float2* din, uint64_t S_in, float2* dout, cu
     return true;
 }
 
+// K7: one persistent CTA per SM; the exchange ring and its counters live in
+// the plan (counters zeroed per launch; launches sharing them are ordered)
+int launch_l2x(ppfg_plan p, const float2* din, uint64_t S_in, float2* dout, cudaStream_t st) {
+    const L2xEntry* e = p->l2x;
+    const size_t ctr_bytes = sizeof(unsigned) * 2 * e->nsr;
+    if (p->ring_bytes < e->ring_bytes + ctr_bytes) {
+        if (p->d_ring) {
+            PPFG_CUDA(cudaStreamSynchronize(st));
+            cudaFree(p->d_ring);
+            p->d_ring = nullptr;
+            p->ring_bytes = 0;
+        }
+        PPFG_CUDA(cudaMalloc(&p->d_ring, e->ring_bytes + ctr_bytes));
+        p->ring_bytes = e->ring_bytes + ctr_bytes;
+    }
+    if (!p->ev_ring)
+        PPFG_CUDA(cudaEventCreateWithFlags(&p->ev_ring, cudaEventDisableTiming));
+    else
+        PPFG_CUDA(cudaStreamWaitEvent(st, p->ev_ring, 0)); // a previous launch on another stream
+    unsigned* ctr = reinterpret_cast<unsigned*>(static_cast<char*>(p->d_ring) + e->ring_bytes);
+    PPFG_CUDA(cudaMemsetAsync(ctr, 0, ctr_bytes, st));
+    PPFG_TRY(ensure_smem_attr(e->fn, e->smem, p->device));
+    CUtensorMap map;
+    PPFG_TRY(encode_rows_map(&map, din, p->C, S_in, 32, e->rb));
+    long long S_out = static_cast<long long>(S_in - p->T + 1);
+    float2* ring = static_cast<float2*>(p->d_ring);
+    void* args[] = {&map, &dout, &ring, &ctr, &S_out, &p->d_taps, &p->d_tw};
+    PPFG_CUDA(cudaLaunchKernel(e->fn, dim3(static_cast<unsigned>(p->num_sms)), dim3(e->nt), args, e->smem, st));
+    PPFG_TRY(check_launch("fused fir+fft kernel (L2 exchange)"));
+    PPFG_CUDA(cudaEventRecord(p->ev_ring, st));
+    return PPFG_OK;
+}
+
 int launch_fir_fft(ppfg_plan p, const float2* din, uint64_t S_in, float2* dout, cudaStream_t st) {
+    if (p->l2x && !(p->flags & PPFG_UNFUSED) && aligned16(din))
+        return launch_l2x(p, din, S_in, dout, st);
     if (p->fused && !(p->flags & PPFG_UNFUSED) && aligned16(din))
         return launch_fused(p, din, S_in, dout, st);
     int rc_tiny = PPFG_OK;
@@ -1235,6 +1281,16 @@ int ppfg_plan_create(ppfg_plan* plan, uint64_t n_channels, uint64_t n_taps,
                 break;
             }
         }
+        for (const auto& e : l2x_entries()) {
+            if (e.L == p->L && e.T == static_cast<int>(n_taps) && e.exact == exact &&
+                (e.preferred || (flags & PPFG_L2X))) {
+                p->l2x = &e;
+                FusedEntry tmp{};
+                tmp.sig = e.sig;
+                p->fused_name = "fused_l2x_kernel<" + kernel_name_of(tmp).substr(std::strlen("fused_fir_fft_kernel<"));
+                break;
+            }
+        }
     }
     *plan = p;
     return PPFG_OK;
@@ -1253,6 +1309,9 @@ int ppfg_plan_destroy(ppfg_plan p) {
     cudaFree(p->d_ones);
     cudaFree(p->d_part);
     cudaFree(p->d_bins);
+    cudaFree(p->d_ring);
+    if (p->ev_ring)
+        cudaEventDestroy(p->ev_ring);
 
     for (int i = 0; i < 2; ++i) {
         cudaFree(p->d_in[i]);
@@ -1285,7 +1344,7 @@ const char* ppfg_fir_fft_kernel_name(ppfg_plan p) {
     if (!(p->flags & PPFG_UNFUSED) && p->L >= 1 && p->L <= 5 && p->T > 0 &&
         tiny_table(p->L, static_cast<int>(p->T), !(p->flags & PPFG_FAST)))
         return p->flags & PPFG_FAST ? "fused_tiny_kernel (FP32 FIR)" : "fused_tiny_kernel (FP64 FIR)";
-    if (!p->fused || (p->flags & PPFG_UNFUSED))
+    if (!(p->l2x || p->fused) || (p->flags & PPFG_UNFUSED))
         return "unfused (FIR kernel + FFT kernel)";
     return p->fused_name.c_str();
 }
@@ -1327,6 +1386,8 @@ int ppfg_fir_fft_kind(ppfg_plan p) {
     if (p && !(p->flags & PPFG_UNFUSED) && p->L >= 1 && p->L <= 5 && p->T > 0 &&
         tiny_table(p->L, static_cast<int>(p->T), !(p->flags & PPFG_FAST)))
         return p->flags & PPFG_FAST ? 5 : 6;
+    if (p && p->l2x && !(p->flags & PPFG_UNFUSED))
+        return p->l2x->exact ? 8 : 7;
     if (!p || !p->fused || (p->flags & PPFG_UNFUSED))
         return 0;
     return (p->fused->exact ? 2 : 1) + (p->fused->q > 1 ? 2 : 0);

@@ -1,0 +1,30 @@
+// tab_l2x.cu — K7 fused FIR + FFT through an L2-resident exchange ring
+// (l2x.cuh): long filters at C = 1024 and the C = 8192 transform.
+#include "tables_impl.cuh"
+
+namespace ppfg {
+
+namespace {
+template <class Cfg>
+L2xEntry l2x_entry(bool preferred) {
+    L2xEntry e{Cfg::L, Cfg::T, Cfg::EXACT, reinterpret_cast<KernelFn>(&fused_l2x_kernel<Cfg>),
+               Cfg::SMEM, Cfg::NT, Cfg::RB, sizeof(float2) * Cfg::RING_SLOT_FLOATS2 * Cfg::NSR,
+               Cfg::NSR, preferred};
+    e.sig = __PRETTY_FUNCTION__;
+    return e;
+}
+} // namespace
+
+std::vector<L2xEntry> l2x_table() {
+    return {
+        l2x_entry<L2xCfg<10, 32, false>>(false),
+        l2x_entry<L2xCfg<10, 64, false, 8, 4, 8, 8>>(false),
+        l2x_entry<L2xCfg<10, 16, false>>(false),
+        l2x_entry<L2xCfg<10, 32, true>>(false),
+        // C = 8192: 64-spectrum chunks (4 MB ring slots), 4 slots
+        l2x_entry<L2xCfg<13, 8, false, 16, 4, 1, 4, 4>>(false),
+        l2x_entry<L2xCfg<13, 8, true, 16, 4, 1, 4, 4>>(false),
+    };
+}
+
+} // namespace ppfg

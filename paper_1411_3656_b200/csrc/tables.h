@@ -73,6 +73,21 @@ FirTmaEntry fir_tma_table(int T);   // K1t, tab_fir.cu
 FirTmaEntry fir_fast_table(int T);  // K1f, tab_fir.cu
 FirBlkEntry fir_blk_table(int T, bool exact); // K1b, tab_fir_blk.cu
 FirEntry fir_table(int T);          // K1, tab_fir.cu
+// K7 fused FIR + FFT through an L2-resident exchange ring (l2x.cuh)
+struct L2xEntry {
+    int L, T;
+    bool exact;
+    KernelFn fn;
+    size_t smem;
+    int nt;
+    int rb;                    // TMA box rows (input chunk)
+    size_t ring_bytes;         // the exchange ring in global memory
+    int nsr;                   // ring slots (counters: 2 * nsr)
+    bool preferred;            // taken by default (measured faster than the alternatives)
+    const char* sig = nullptr; // __PRETTY_FUNCTION__ of the entry maker
+};
+std::vector<L2xEntry> l2x_table(); // tab_l2x.cu
+
 // K6 fused FIR+FFT for C = 2^L, L = 1..5 (tiny.cuh), tab_tiny.cu; nullptr
 // where no instantiation covers (L, T, exact)
 KernelFn tiny_table(int L, int T, bool exact);

@@ -10,6 +10,7 @@
 #include "fused.cuh"
 #include "fused_split.cuh"
 #include "tiny.cuh"
+#include "l2x.cuh"
 
 namespace ppfg {
 

@@ -22,6 +22,7 @@ UNFUSED = 2
 CLUSTER = 4
 K1_PREFETCH = 8  # comparison only: register-prefetch FIR kernel
 FIR_LEGACY = 16  # comparison only: lane-window FIR kernels instead of K1b
+L2X = 32  # also admit the L2-exchange fused kernels (K7) not taken by default
 MEM_HOST = 0
 MEM_DEVICE = 1
 

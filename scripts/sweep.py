@@ -60,7 +60,7 @@ def point(C, T, gib, peak):
             t = timeit(lambda: p.fir_fft(x, out=y))
             res[mode] = {"ms": t * 1e3, "gbs_in": bin_ / t / 1e9,
                          "frac": (bin_ + bout) / t / 1e9 / peak,
-                         "kernel": ["unfused", "fused-fp32", "fused-fp64", "cluster-fp32", "cluster-fp64", "tiny-fp32", "tiny-fp64"][p.kind]}
+                         "kernel": ["unfused", "fused-fp32", "fused-fp64", "cluster-fp32", "cluster-fp64", "tiny-fp32", "tiny-fp64", "l2x-fp32", "l2x-fp64"][p.kind]}
     with ppf.Plan(C, T, coeffs, flags=ppf.FAST) as p:
         # detection (mean power per channel): only the input is HBM traffic
         # when a fused detection kernel exists

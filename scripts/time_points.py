@@ -9,7 +9,8 @@ from scripts.sweep import timeit
 import bench
 peak, _ = bench.measured_peak()
 FL = {"fast": ppf.FAST, "exact": ppf.EXACT, "fast-unfused": ppf.FAST | ppf.UNFUSED,
-      "fast-cluster": ppf.FAST | ppf.CLUSTER, "exact-unfused": ppf.UNFUSED}
+      "fast-cluster": ppf.FAST | ppf.CLUSTER, "exact-unfused": ppf.UNFUSED,
+      "fast-l2x": ppf.FAST | ppf.L2X, "exact-l2x": ppf.EXACT | ppf.L2X}
 tag = os.environ.get("TAG", "")
 for spec in sys.argv[1:]:
     C, T, mode = spec.split(":")

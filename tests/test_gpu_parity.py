@@ -264,6 +264,31 @@ def test_tiny_c_fused_vs_oracle(cuda, port, C, T, mode):
             assert kind == (6 if mode == "exact" else 5)
 
 
+@pytest.mark.parametrize("C,T,mode", [(1024, 32, "fast"), (1024, 64, "fast"), (1024, 16, "fast"),
+                                      (1024, 32, "exact"), (8192, 8, "fast"), (8192, 8, "exact")])
+def test_l2x_fused_vs_oracle(cuda, port, C, T, mode):
+    """K7 (l2x.cuh): FIR -> L2-resident exchange ring -> FFT in one persistent
+    kernel. EXACT bit-identical, FAST within the north-star bar; a single
+    output, chunk-ragged tails, a multi-round run (more work items than SMs),
+    and repeated launches on one plan (the ring and counters are reused)."""
+    ppf = ppf_mod()
+    coeffs = port.generate_prototype(C, T, 9.0)
+    flags = (ppf.EXACT if mode == "exact" else ppf.FAST) | ppf.L2X
+    sizes = (T, T + 300, T + 4000) if C == 8192 else (T, T + 255, T + 256, T + 3 * 256 * 148 // 32 + 17)
+    with ppf.Plan(C, T, coeffs, flags=flags) as p:
+        assert p.kind == (8 if mode == "exact" else 7), p.kernel_name
+        for S in sizes:
+            x = ppf.synth(C, S * C, seed=S + T)
+            want = port.fir_fft(x, C, T, coeffs).view(np.complex64)
+            for rep in range(2):
+                got = p.fir_fft(x)
+                assert got.shape == (S - T + 1, C)
+                if mode == "exact":
+                    assert np.array_equal(bits(got), bits(want)), (S, rep)
+                else:
+                    assert max_err_over_rms(got, want) <= 1e-5 * np.log2(C), (S, rep)
+
+
 @pytest.mark.parametrize("S_extra", [0, 1, 2, 7, 8, 9, 100])
 def test_fused_small_and_ragged(cuda, port, S_extra):
     """n_spectra_out = 1 and tails that do not fill a batch (SURVEY §7 hard part 7)."""
