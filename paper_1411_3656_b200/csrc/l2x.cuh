@@ -16,8 +16,8 @@
 //    registers, each output accumulated in ascending tap order — FP64 from
 //    h0*x0 in EXACT mode, bit-identical to ppf_fir_optimized, fir.hpp:85-110;
 //    FP32 FFMA2 in FAST mode). The outputs go to ring slot k mod NSR (plain
-//    stores, L2), then the item is published: __threadfence by every thread,
-//    a role barrier, one release add on produced[slot].
+//    stores, L2), then the item is published: a role barrier, then one
+//    GPU-scope release add on produced[slot].
 //  FFT role (NFFT warps): tile (k, i) = BT consecutive spectra of chunk k, tile
 //    j on CTA j mod grid. Its leader waits (acquire spin) until all C/32 items
 //    of chunk k are published, the first pass loads the rows from the ring
@@ -44,8 +44,8 @@
 
 namespace ppfg {
 
-template <int L_, int T_, bool EXACT_, int U_ = 16, int NWF_ = 4, int CSR_ = 4, int NS_ = 6,
-          int NSR_ = 8, int NWT_ = 8, int W_ = 5, int FIR_REGS_ = 168, int FFT_REGS_ = 128>
+template <int L_, int T_, bool EXACT_, int U_ = 8, int NWF_ = 8, int CSR_ = 4, int NS_ = 6,
+          int NSR_ = 8, int NWT_ = 8, int W_ = 5, int FIR_REGS_ = 160, int FFT_REGS_ = 96>
 struct L2xCfg {
     static constexpr int L = L_, T = T_, N = 1 << L;
     static constexpr bool EXACT = EXACT_;
@@ -279,9 +279,9 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
                 dst[static_cast<size_t>(r0 + u) * N] = y;
             }
         }
-        // publish the item: every thread's ring stores are visible at GPU
-        // scope before the release add
-        __threadfence();
+        // publish the item: the role barrier orders every FIR thread's ring
+        // stores before the leader's GPU-scope release add (the CUTLASS
+        // semaphore pattern: bar.sync, then one st/red.release.gpu)
         named_sync(BAR_FIR, NFIR);
         if (tid == 0) {
             red_release_gpu_add(produced + slot, 1);

@@ -17,13 +17,15 @@ L2xEntry l2x_entry(bool preferred) {
 
 std::vector<L2xEntry> l2x_table() {
     return {
+        // 8 FIR warps x 8 outputs per step (64-row TMA chunks), 256-spectrum
+        // work items, 8 ring slots (16 MB); 8 FFT warps
         l2x_entry<L2xCfg<10, 32, false>>(false),
-        l2x_entry<L2xCfg<10, 64, false, 8, 4, 8, 8>>(false),
+        l2x_entry<L2xCfg<10, 64, false>>(false),
         l2x_entry<L2xCfg<10, 16, false>>(false),
         l2x_entry<L2xCfg<10, 32, true>>(false),
-        // C = 8192: 64-spectrum chunks (4 MB ring slots), 4 slots
-        l2x_entry<L2xCfg<13, 8, false, 16, 4, 1, 4, 4>>(false),
-        l2x_entry<L2xCfg<13, 8, true, 16, 4, 1, 4, 4>>(false),
+        // C = 8192: 64-spectrum items (4 MB ring slots), 4 slots, 4-chunk input ring
+        l2x_entry<L2xCfg<13, 8, false, 8, 8, 1, 4, 4>>(false),
+        l2x_entry<L2xCfg<13, 8, true, 8, 8, 1, 4, 4>>(false),
     };
 }
 
