@@ -61,7 +61,12 @@ struct L2xCfg {
     static constexpr int NFFT = 32 * NWT_, NT = NFIR + NFFT;
     static constexpr int W = W_;
     static constexpr int WMAX = FftSchedule<L, W>::width(0);
-    static constexpr int BT = (NFFT << WMAX) / N > 0 ? (NFFT << WMAX) / N : 1; // spectra per FFT tile
+    // the FFT role is FG independent groups of NFFT / FG threads (one
+    // warpgroup each), each with its own tile: one group's ring loads overlap
+    // the other's passes
+    static constexpr int FG = NWT_ % 8 == 0 ? 2 : 1;
+    static constexpr int FNT = NFFT / FG;        // threads per FFT group
+    static constexpr int BT = (FNT << WMAX) / N > 0 ? (FNT << WMAX) / N : 1; // spectra per FFT tile
     static constexpr int TPC = CS / BT;           // FFT tiles per chunk
     static constexpr int FIR_REGS = FIR_REGS_, FFT_REGS = FFT_REGS_;
     static constexpr unsigned STRIDE = sw_row_stride(N);
@@ -70,7 +75,7 @@ struct L2xCfg {
     static constexpr size_t RING_OFF = (TW_BYTES + 127) & ~size_t(127);
     static constexpr size_t TILE_OFF = RING_OFF + CHUNK_BYTES * NS;
     static constexpr size_t TILE_BYTES = sizeof(float2) * size_t(BT) * STRIDE;
-    static constexpr size_t BAR_OFF = (TILE_OFF + TILE_BYTES + 7) & ~size_t(7);
+    static constexpr size_t BAR_OFF = (TILE_OFF + FG * TILE_BYTES + 7) & ~size_t(7);
     static constexpr size_t SMEM = BAR_OFF + sizeof(uint64_t) * NS;
     static constexpr size_t RING_SLOT_FLOATS2 = size_t(CS) * N; // one L2 ring slot
     static constexpr int LAUNCH_REGS = (65536 / NT) & ~7;
@@ -140,25 +145,29 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
         // ================================ FFT role ================================
         if constexpr (Cfg::FFT_REGS < Cfg::LAUNCH_REGS)
             asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(Cfg::FFT_REGS));
-        const int ftid = tid - NFIR;
-        constexpr int BAR_FFT = 2; // named barrier of the FFT warps
+        constexpr int FG = Cfg::FG, FNT = Cfg::FNT;
+        const int fg = (tid - NFIR) / FNT;         // FFT group
+        const int ftid = tid - NFIR - fg * FNT;
+        const int BAR_FFT = 2 + fg;                // named barrier of the group
+        float2* gtile = tile + fg * (Cfg::TILE_BYTES / sizeof(float2));
         const long long n_tiles = n_chunks * TPC;
-        for (long long j = blockIdx.x; j < n_tiles; j += grid) {
+        // this CTA's tiles blockIdx.x + m * grid, m = fg, fg + FG, ...
+        for (long long j = blockIdx.x + fg * grid; j < n_tiles; j += FG * grid) {
             const long long k = j / TPC;
             const int slot = static_cast<int>(k % NSR);
             const unsigned epoch = static_cast<unsigned>(k / NSR);
             if (ftid == 0)
                 spin_until_geq(produced + slot, (epoch + 1) * NCB); // chunk k published
-            named_sync(BAR_FFT, NFFT);
+            named_sync(BAR_FFT, FNT);
             const long long row0 = k * CS + (j - k * TPC) * BT;
             // ring row (slot, r) == gin + (k*CS + r) * N
             const float2* gin = ring + slot * Cfg::RING_SLOT_FLOATS2 - k * CS * static_cast<long long>(N);
-            FftPasses<L, L, Cfg::W, true, true, NFFT>::run(gin, out, tile, Cfg::STRIDE, BT,
-                                                          L2xRows{row0, S_out}, tw, ftid,
-                                                          SyncNamed{BAR_FFT, NFFT});
+            FftPasses<L, L, Cfg::W, true, true, FNT>::run(gin, out, gtile, Cfg::STRIDE, BT,
+                                                         L2xRows{row0, S_out}, tw, ftid,
+                                                         SyncNamed{BAR_FFT, FNT});
             // every thread's ring loads completed in the first pass (before
             // its barrier); release the tile's rows and the smem tile
-            named_sync(BAR_FFT, NFFT);
+            named_sync(BAR_FFT, FNT);
             if (ftid == 0)
                 red_release_gpu_add(consumed + slot, BT);
         }

@@ -18,11 +18,13 @@ L2xEntry l2x_entry(bool preferred) {
 std::vector<L2xEntry> l2x_table() {
     return {
         // 8 FIR warps x 8 outputs per step (64-row TMA chunks), 256-spectrum
-        // work items, 8 ring slots (16 MB); 8 FFT warps
-        l2x_entry<L2xCfg<10, 32, false>>(false),
-        l2x_entry<L2xCfg<10, 64, false>>(false),
-        l2x_entry<L2xCfg<10, 16, false>>(false),
-        l2x_entry<L2xCfg<10, 32, true>>(false),
+        // work items; 8 FFT warps. Ring slots: the FIR role's round (one item
+        // per CTA) fills grid / (C/32) = 4.6 chunks and the FFT role trails it
+        // by a round, so 16 slots (32 MB) keep both roles busy
+        l2x_entry<L2xCfg<10, 32, false, 8, 8, 4, 6, 16>>(false),
+        l2x_entry<L2xCfg<10, 64, false, 8, 8, 4, 6, 16>>(false),
+        l2x_entry<L2xCfg<10, 16, false, 8, 8, 4, 6, 16>>(false),
+        l2x_entry<L2xCfg<10, 32, true, 8, 8, 4, 6, 16>>(false),
         // C = 8192: 64-spectrum items (4 MB ring slots), 4 slots, 4-chunk input ring
         l2x_entry<L2xCfg<13, 8, false, 8, 8, 1, 4, 4>>(false),
         l2x_entry<L2xCfg<13, 8, true, 8, 8, 1, 4, 4>>(false),
