@@ -45,7 +45,7 @@
 namespace ppfg {
 
 template <int L_, int T_, bool EXACT_, int U_ = 8, int NWF_ = 8, int CSR_ = 4, int NS_ = 6,
-          int NSR_ = 8, int NWT_ = 8, int W_ = 5, int FIR_REGS_ = 160, int FFT_REGS_ = 96>
+          int NSR_ = 8, int NWT_ = 8, int W_ = 5, int FIR_REGS_ = 160, int FFT_REGS_ = 96, int FG_ = 2>
 struct L2xCfg {
     static constexpr int L = L_, T = T_, N = 1 << L;
     static constexpr bool EXACT = EXACT_;
@@ -64,7 +64,7 @@ struct L2xCfg {
     // the FFT role is FG independent groups of NFFT / FG threads (one
     // warpgroup each), each with its own tile: one group's ring loads overlap
     // the other's passes
-    static constexpr int FG = NWT_ % 8 == 0 ? 2 : 1;
+    static constexpr int FG = FG_;
     static constexpr int FNT = NFFT / FG;        // threads per FFT group
     static constexpr int BT = (FNT << WMAX) / N > 0 ? (FNT << WMAX) / N : 1; // spectra per FFT tile
     static constexpr int TPC = CS / BT;           // FFT tiles per chunk
@@ -80,6 +80,7 @@ struct L2xCfg {
     static constexpr size_t RING_SLOT_FLOATS2 = size_t(CS) * N; // one L2 ring slot
     static constexpr int LAUNCH_REGS = (65536 / NT) & ~7;
     static_assert(N >= 32 && CS % BT == 0, "whole FFT tiles per chunk");
+    static_assert(NWT_ % (4 * FG_) == 0, "FFT groups of whole warpgroups");
     static_assert(NS >= NEED + 1, "input ring: a step's chunks plus lookahead");
     static_assert((RB & (RB - 1)) == 0 && RB <= 256, "power-of-two chunks within a TMA box");
     static_assert(FIR_REGS * NFIR + FFT_REGS * NFFT <= LAUNCH_REGS * NT, "register split");

@@ -26,8 +26,9 @@ std::vector<L2xEntry> l2x_table() {
         l2x_entry<L2xCfg<10, 16, false, 8, 8, 4, 6, 16>>(false),
         l2x_entry<L2xCfg<10, 32, true, 8, 8, 4, 6, 16>>(false),
         // C = 8192: 64-spectrum items (4 MB ring slots), 4 slots, 4-chunk input ring
-        l2x_entry<L2xCfg<13, 8, false, 8, 8, 1, 4, 4>>(false),
-        l2x_entry<L2xCfg<13, 8, true, 8, 8, 1, 4, 4>>(false),
+        // (one FFT group: two 8192-point tiles do not fit next to the twiddles)
+        l2x_entry<L2xCfg<13, 8, false, 8, 8, 1, 4, 4, 8, 5, 160, 96, 1>>(false),
+        l2x_entry<L2xCfg<13, 8, true, 8, 8, 1, 4, 4, 8, 5, 160, 96, 1>>(false),
     };
 }
 
