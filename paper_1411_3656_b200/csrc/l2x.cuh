@@ -16,8 +16,8 @@
 //    registers, each output accumulated in ascending tap order — FP64 from
 //    h0*x0 in EXACT mode, bit-identical to ppf_fir_optimized, fir.hpp:85-110;
 //    FP32 FFMA2 in FAST mode). The outputs go to ring slot k mod NSR (plain
-//    stores, L2), then the item is published: a role barrier, then one
-//    GPU-scope release add on produced[slot].
+//    stores, L2), then each warp publishes its part with one GPU-scope
+//    release add on produced[slot].
 //  FFT role (NFFT warps): tile (k, i) = BT consecutive spectra of chunk k, tile
 //    j on CTA j mod grid. Its leader waits (acquire spin) until all C/32 items
 //    of chunk k are published, the first pass loads the rows from the ring
@@ -157,8 +157,8 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
             const long long k = j / TPC;
             const int slot = static_cast<int>(k % NSR);
             const unsigned epoch = static_cast<unsigned>(k / NSR);
-            if (ftid == 0)
-                spin_until_geq(produced + slot, (epoch + 1) * NCB); // chunk k published
+            if (ftid == 0) // chunk k published: every FIR warp of its C/32 items
+                spin_until_geq(produced + slot, (epoch + 1) * NCB * Cfg::NWF);
             named_sync(BAR_FFT, FNT);
             const long long row0 = k * CS + (j - k * TPC) * BT;
             // ring row (slot, r) == gin + (k*CS + r) * N
@@ -169,8 +169,9 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
             // every thread's ring loads completed in the first pass (before
             // its barrier); release the tile's rows and the smem tile
             named_sync(BAR_FFT, FNT);
-            if (ftid == 0)
-                red_release_gpu_add(consumed + slot, BT);
+            if (ftid == 0) // relaxed: the loads it vouches for have returned their values
+                asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(consumed + slot), "r"(BT)
+                             : "memory");
         }
         return;
     }
@@ -289,16 +290,17 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
                 dst[static_cast<size_t>(r0 + u) * N] = y;
             }
         }
-        // publish the item: the role barrier orders every FIR thread's ring
-        // stores before the leader's GPU-scope release add (the CUTLASS
-        // semaphore pattern: bar.sync, then one st/red.release.gpu)
-        named_sync(BAR_FIR, NFIR);
-        if (tid == 0) {
+        // publish the item per warp: the warp's ring stores, then one
+        // GPU-scope release add by its lane 0 (the FFT role waits for
+        // NWF * C/32 of them per chunk) — a release waits for the releasing
+        // warp's own stores only, so the warps do not serialise on one fence
+        __syncwarp();
+        if (lane == 0)
             red_release_gpu_add(produced + slot, 1);
-            // the item's remaining input chunks are released: refill
+        named_sync(BAR_FIR, NFIR); // every warp is done with the item's input chunks
+        if (tid == 0) // refill the released slots
             for (; issued < my_chunks && issued < g0 + NIC + NS; ++issued)
                 issue(issued);
-        }
     }
 }
 
