@@ -42,6 +42,10 @@
 
 #include "fused.cuh"
 
+#ifndef PPFG_L2X_DEBUG
+#define PPFG_L2X_DEBUG 0 // timing experiments only: 1 = FIR role skips its math, 2 = FFT role skips its passes
+#endif
+
 namespace ppfg {
 
 template <int L_, int T_, bool EXACT_, int U_ = 8, int NWF_ = 8, int CSR_ = 4, int NS_ = 6,
@@ -163,9 +167,11 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
             const long long row0 = k * CS + (j - k * TPC) * BT;
             // ring row (slot, r) == gin + (k*CS + r) * N
             const float2* gin = ring + slot * Cfg::RING_SLOT_FLOATS2 - k * CS * static_cast<long long>(N);
+#if PPFG_L2X_DEBUG != 2
             FftPasses<L, L, Cfg::W, true, true, FNT>::run(gin, out, gtile, Cfg::STRIDE, BT,
                                                          L2xRows{row0, S_out}, tw, ftid,
                                                          SyncNamed{BAR_FFT, FNT});
+#endif
             // every thread's ring loads completed in the first pass (before
             // its barrier); release the tile's rows and the smem tile
             named_sync(BAR_FFT, FNT);
@@ -238,6 +244,14 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
                     for (; issued < my_chunks && issued < g0 + st + NS; ++issued) // chunk g reuses the slot of g - NS
                         issue(issued);
             }
+#if PPFG_L2X_DEBUG == 1
+            if (true) {
+                const long long need0 = min(g0 + st + NEED - 1, g0 + NIC - 1);
+                for (; waited <= need0; ++waited)
+                    mbar_wait(full + static_cast<int>(waited % NS), static_cast<uint32_t>((waited / NS) & 1));
+                continue;
+            }
+#endif
             const long long need = min(g0 + st + NEED - 1, g0 + NIC - 1);
             for (; waited <= need; ++waited)
                 mbar_wait(full + static_cast<int>(waited % NS), static_cast<uint32_t>((waited / NS) & 1));
