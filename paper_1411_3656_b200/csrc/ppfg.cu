@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <list>
 #include <map>
 #include <mutex>
 #include <string>
@@ -691,10 +692,13 @@ bool launch_tiny(ppfg_plan p, const float2* din, uint64_t S_in, float2* dout, cu
     if (!fn)
         return false;
     const uint64_t T = p->T, S_out = S_in - T + 1;
+    // tiny.cuh: the step loop's unroll max(T, PF) (segments are whole unrolls)
+    const bool pf16 = T == 16 || (T == 8 && (!(p->flags & PPFG_FAST) || p->L <= 3));
+    const uint64_t unroll = std::max<uint64_t>(T, pf16 ? 16 : 8);
     const uint64_t groups_per_warp = 32 >> p->L;
     const uint64_t target = static_cast<uint64_t>(p->num_sms) * 48 * 4 * groups_per_warp;
     uint64_t seg = std::max<uint64_t>(cdiv(S_out, target), std::min<uint64_t>(S_out, 4 * T));
-    seg = cdiv(seg, T) * T;
+    seg = cdiv(seg, unroll) * unroll;
     const long long n_tasks = static_cast<long long>(cdiv(S_out, seg));
     const uint64_t warps = cdiv(static_cast<uint64_t>(n_tasks), groups_per_warp);
     long long S_in_ll = static_cast<long long>(S_in), S_out_ll = static_cast<long long>(S_out);
@@ -1159,6 +1163,59 @@ std::string kernel_name_of(const FusedEntry& e) {
     return std::string(e.q > 1 ? "fused_split_kernel<" : "fused_fir_fft_kernel<") + cfg + ">";
 }
 
+// Process-wide cache of idle plans for the library's own one-shot entry
+// points (ppfg_multi_fir_fft's per-device shards, the single-row fft /
+// dft_naive helpers): keyed by (device, C, T, flags, coefficient values);
+// a plan is leased to one call at a time and keeps its pinned staging and
+// device buffers between calls. At most kMaxIdle idle plans are kept.
+struct PlanLease {
+    int device = 0;
+    uint64_t C = 0, T = 0;
+    uint32_t flags = 0;
+    std::vector<double> values;
+    ppfg_plan plan = nullptr;
+};
+struct LibPlanCache {
+    static constexpr size_t kMaxIdle = 16;
+    std::mutex mu;
+    std::list<PlanLease> idle; // most recently used first
+};
+LibPlanCache& lib_plan_cache() {
+    static LibPlanCache* c = new LibPlanCache(); // never destroyed: no exit-order issues
+    return *c;
+}
+int lease_plan(uint64_t C, uint64_t T, const double* values, uint32_t flags, int device, PlanLease* out) {
+    out->device = device;
+    out->C = C;
+    out->T = T;
+    out->flags = flags;
+    out->values.assign(values, values + (T ? C * T : 0));
+    {
+        auto& c = lib_plan_cache();
+        std::lock_guard<std::mutex> lk(c.mu);
+        for (auto it = c.idle.begin(); it != c.idle.end(); ++it) {
+            if (it->device == device && it->C == C && it->T == T && it->flags == flags &&
+                it->values == out->values) {
+                out->plan = it->plan;
+                c.idle.erase(it);
+                return PPFG_OK;
+            }
+        }
+    }
+    return ppfg_plan_create(&out->plan, C, T, T ? out->values.data() : nullptr, flags, device);
+}
+void return_plan(PlanLease&& l) {
+    if (!l.plan)
+        return;
+    auto& c = lib_plan_cache();
+    std::lock_guard<std::mutex> lk(c.mu);
+    c.idle.push_front(std::move(l));
+    while (c.idle.size() > LibPlanCache::kMaxIdle) {
+        ppfg_plan_destroy(c.idle.back().plan);
+        c.idle.pop_back();
+    }
+}
+
 } // namespace
 
 // ================================================================ C-ABI
@@ -1455,8 +1512,9 @@ static int one_row(const void* in, uint64_t n, void* out, bool fallback, const c
         return fail(PPFG_UNSUPPORTED_SIZE, "fft: size must be a power of two");
     int dev = 0;
     cudaGetDevice(&dev);
-    ppfg_plan p = nullptr;
-    PPFG_TRY(ppfg_plan_create(&p, n, 0, nullptr, 0, dev));
+    PlanLease lease;
+    PPFG_TRY(lease_plan(n, 0, nullptr, 0, dev, &lease));
+    ppfg_plan p = lease.plan;
     int rc;
     if (fallback && is_pow2(n) && n > 1) { // force the naive path for dft_naive
         DeviceGuard dg(p->device);
@@ -1480,7 +1538,7 @@ static int one_row(const void* in, uint64_t n, void* out, bool fallback, const c
     } else {
         rc = ppfg_channelize(p, in, 1, out, fallback ? 1 : 0, PPFG_MEM_HOST, nullptr);
     }
-    ppfg_plan_destroy(p);
+    return_plan(std::move(lease));
     return rc;
 }
 
@@ -1525,16 +1583,17 @@ int ppfg_multi_fir_fft(uint64_t n_channels, uint64_t n_taps, const double* coeff
         pool.emplace_back([&, g]() {
             uint64_t ib, ic, ob, oc;
             int st = ppfg_shard_range(n_spectra_in, n_taps, g, n_devices, &ib, &ic, &ob, &oc);
-            ppfg_plan p = nullptr;
+            // per-device plans (and their pinned staging) persist across calls
+            PlanLease lease;
             if (st == PPFG_OK && oc > 0)
-                st = ppfg_plan_create(&p, n_channels, n_taps, coeff_values, flags, devices[g]);
+                st = lease_plan(n_channels, n_taps, coeff_values, flags, devices[g], &lease);
             if (st == PPFG_OK && oc > 0)
-                st = ppfg_fir_fft(p, static_cast<const char*>(host_in) + ib * row_bytes, ic,
+                st = ppfg_fir_fft(lease.plan, static_cast<const char*>(host_in) + ib * row_bytes, ic,
                                   static_cast<char*>(host_out) + ob * row_bytes, PPFG_MEM_HOST,
                                   nullptr);
             if (st != PPFG_OK)
                 msgs[g] = g_err;
-            ppfg_plan_destroy(p);
+            return_plan(std::move(lease));
             status[g] = st;
         });
     }

@@ -18,7 +18,7 @@
 //   - after the last stage lane c holds bin rev_L(c) and stores it: the group
 //     writes its C-bin row as one contiguous (permuted) segment.
 // Inputs are read through a register prefetch queue: the load of step
-// tau + min(T, 8) is issued at step tau, so that many rows per lane are in
+// tau + PF (8 or 16) is issued at step tau, so that many rows per lane are in
 // flight while the window filters.
 #pragma once
 
@@ -76,17 +76,24 @@ __global__ void __launch_bounds__(256) fused_tiny_kernel(const float2* __restric
         xw[t].x = x.x;
         xw[t].y = x.y;
     }
-    // prefetch queue: the input of step tau + PF is loaded at step tau
-    constexpr int PF = T < 8 ? T : 8;
-    static_assert(T % PF == 0, "prefetch depth divides the unroll");
+    // prefetch queue: the input of step tau + PF is loaded at step tau (16
+    // rows in flight per lane; 8 at T = 32, where the window is large); the
+    // step loop is unrolled by UNR = max(T, PF) so both the window slot and
+    // the queue slot are compile-time
+    // (measured at 1 GiB: 16 rows ahead helped every T = 16 shape and T = 8 at
+    // C <= 8 or in FP64 — C=8 T=8 FP64 0.58 -> 0.70, C=16 T=16 0.57 -> 0.63 —
+    // but not C=32 T=8 FP32 (0.735 -> 0.69) nor C=2 T=4 FP64 (0.51 -> 0.44))
+    constexpr int PF = (T == 16 || (T == 8 && (EXACT || L <= 3))) ? 16 : 8;
+    constexpr int UNR = T > PF ? T : PF;
+    static_assert(UNR % T == 0 && UNR % PF == 0, "window and queue cycles divide the unroll");
     float2 nx[PF];
 #pragma unroll
     for (int u = 0; u < PF; ++u)
         nx[u] = ld(s0 + T - 1 + u);
 
-    for (int tau0 = 0; tau0 < seg; tau0 += T) {
+    for (int tau0 = 0; tau0 < seg; tau0 += UNR) {
 #pragma unroll
-        for (int u = 0; u < T; ++u) {
+        for (int u = 0; u < UNR; ++u) {
             // newest input of this step -> circular slot (u + T - 1) % T
             const float2 x = nx[u % PF];
             nx[u % PF] = ld(s0 + tau0 + u + PF + T - 1);
