@@ -336,7 +336,9 @@ def ncu_traffic(C, T, mode, n_spectra_in, kernel_name):
             t = json.load(open(f))
         except (OSError, ValueError):
             continue
-        cfg = kernel_name[kernel_name.find("<") + 1:] if "<" in kernel_name else kernel_name
+        # "fused_fir_fft_kernel<FusedCfg<...>>" -> "FusedCfg<...>", a substring of
+        # ncu's "void fused_fir_fft_kernel<FusedCfg<...>, 0>(...)"
+        cfg = kernel_name[kernel_name.find("<") + 1:-1] if "<" in kernel_name else kernel_name
         if (t.get("n_channels"), t.get("n_taps"), t.get("mode"), t.get("n_spectra_in")) == \
                 (C, T, mode, n_spectra_in) and cfg and cfg in t.get("kernel", ""):
             return t["traffic_per_launch"], os.path.relpath(f, ROOT)
@@ -565,6 +567,9 @@ def main():
                                   "peak": peak, "unit": "GB/s",
                                   "frac": alg_bytes / te_launch / 1e9 / peak,
                                   "launch_ms": te_launch * 1e3}}
+            tr, tr_src = ncu_traffic(C, T, "exact", ic, pe.kernel_name)
+            exact["roofline"]["traffic"] = tr
+            exact["roofline"]["traffic_source"] = tr_src
 
     # ---- parity: every output spectrum of the timed runs vs the reference ----
     parity = None
