@@ -8,7 +8,9 @@ std::vector<FusedEntry> fused_part_split() {
     // argument) where it measured faster (1 GiB): C=1024 T=16 0.645 -> 0.70,
     // EXACT C=1024 T=8 0.63 -> 0.645 (6.5 GB SKA EXACT 0.668 -> 0.682), EXACT
     // T=16 0.403 -> 0.411, C=2048 0.69 -> 0.71, C=4096 0.533 -> 0.537, T=32
-    // 0.416 -> 0.420; not EXACT C=2048 (0.474 -> 0.463).
+    // 0.416 -> 0.420; not EXACT C=2048 (0.474 -> 0.463). Register splits with
+    // HS (two A/B rounds): C=4096 FIR/FFT 168/88 0.537 -> 0.562; 128/128 and
+    // 144/112 elsewhere, and flipping the float4 twiddles, all measured slower.
     return {
         // thread-block clusters, FIR split by channel block and FFT by
         // spectrum (fused_split.cuh) — for FIR state that does not fit one SM.
@@ -35,7 +37,7 @@ std::vector<FusedEntry> fused_part_split() {
         split_entry<SplitCfg<10, 2, 16, true, 2, 5, 152, 104, 0, true, true>>(true),
         split_entry<SplitCfg<11, 1, 8, false, 2, 5, 136, 120, 0, false, true>>(true),
         split_entry<SplitCfg<11, 2, 8, true, 2, 5, 152, 104, 0, true>>(true),
-        split_entry<SplitCfg<12, 2, 8, false, 2, 5, 152, 104, 0, false, true>>(true),
+        split_entry<SplitCfg<12, 2, 8, false, 2, 5, 168, 88, 0, false, true>>(true),
         split_entry<SplitCfg<13, 3, 8, false>>(false),
     };
 }
