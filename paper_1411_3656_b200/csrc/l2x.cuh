@@ -43,13 +43,15 @@
 #include "fused.cuh"
 
 #ifndef PPFG_L2X_DEBUG
-#define PPFG_L2X_DEBUG 0 // timing experiments only: 1 = FIR role skips its math, 2 = FFT role skips its passes
+#define PPFG_L2X_DEBUG 0 // timing experiments only: 1 = FIR role skips its math, 2 = FFT role skips its
+                         // passes, 3 = FIR role skips its ring stores
 #endif
 
 namespace ppfg {
 
 template <int L_, int T_, bool EXACT_, int U_ = 8, int NWF_ = 8, int CSR_ = 4, int NS_ = 6,
-          int NSR_ = 8, int NWT_ = 8, int W_ = 5, int FIR_REGS_ = 160, int FFT_REGS_ = 96, int FG_ = 2>
+          int NSR_ = 8, int NWT_ = 8, int W_ = 5, int FIR_REGS_ = 160, int FFT_REGS_ = 96, int FG_ = 2,
+          int NSLOT_ = 2>
 struct L2xCfg {
     static constexpr int L = L_, T = T_, N = 1 << L;
     static constexpr bool EXACT = EXACT_;
@@ -78,12 +80,19 @@ struct L2xCfg {
     static constexpr size_t TW_BYTES = sizeof(float2) * N;
     static constexpr size_t RING_OFF = (TW_BYTES + 127) & ~size_t(127);
     static constexpr size_t TILE_OFF = RING_OFF + CHUNK_BYTES * NS;
-    static constexpr size_t TILE_BYTES = sizeof(float2) * size_t(BT) * STRIDE;
-    static constexpr size_t BAR_OFF = (TILE_OFF + FG * TILE_BYTES + 7) & ~size_t(7);
-    static constexpr size_t SMEM = BAR_OFF + sizeof(uint64_t) * NS;
+    // an FFT group's tile slots: rows land there by TMA bulk copies in natural
+    // order and are transformed in place (the first pass rewrites them at
+    // swizzled slots); NSLOT = 2 overlaps a tile's copies with the previous
+    // tile's passes
+    static constexpr int NSLOT = NSLOT_;
+    static constexpr size_t TILE_BYTES = (sizeof(float2) * size_t(BT) * STRIDE + 127) & ~size_t(127);
+    static constexpr size_t BAR_OFF = (TILE_OFF + size_t(FG) * NSLOT * TILE_BYTES + 7) & ~size_t(7);
+    static constexpr size_t SMEM = BAR_OFF + sizeof(uint64_t) * (NS + FG * NSLOT);
     static constexpr size_t RING_SLOT_FLOATS2 = size_t(CS) * N; // one L2 ring slot
     static constexpr int LAUNCH_REGS = (65536 / NT) & ~7;
     static_assert(N >= 32 && CS % BT == 0, "whole FFT tiles per chunk");
+    static_assert(FftSchedule<L, W_>::NP >= 2, "the first pass hands over to FftPasses<.., I = 1>");
+    static_assert((sizeof(float2) * STRIDE) % 16 == 0, "bulk-copy destinations 16-byte aligned");
     static_assert(NWT_ % (4 * FG_) == 0, "FFT groups of whole warpgroups");
     static_assert(NS >= NEED + 1, "input ring: a step's chunks plus lookahead");
     static_assert((RB & (RB - 1)) == 0 && RB <= 256, "power-of-two chunks within a TMA box");
@@ -110,6 +119,19 @@ PPFG_DEV void spin_until_geq(const unsigned* p, unsigned target) {
     }
 }
 
+// Debug timeline (PPFG_L2X_TRACE, host side): when ctr[2*NSR] != 0, CTA 0
+// records %globaltimer at role events into ctr + 64 (u64 [2 roles][8][256]).
+PPFG_DEV unsigned long long l2x_now() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define L2X_TR(role, ev, i)                                                                       \
+    do {                                                                                          \
+        if (tracing && (i) < 256)                                                                 \
+            trace[((role) * 8 + (ev)) * 256 + (i)] = l2x_now();                                   \
+    } while (0)
+
 // Output rows of an FFT tile: spectra row0 .. row0 + BT - 1 (k*CS + i*BT),
 // -1 past the end. The ring is addressed through the same row index: the
 // caller shifts the ring pointer by -row_of_slot so gin + row * N lands in
@@ -134,6 +156,8 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + Cfg::BAR_OFF);
     unsigned* produced = ctr;        // [NSR]: items published per slot (all epochs)
     unsigned* consumed = ctr + NSR;  // [NSR]: rows read per slot (all epochs)
+    const bool tracing = blockIdx.x == 0 && ctr[2 * NSR] != 0;
+    unsigned long long* trace = reinterpret_cast<unsigned long long*>(ctr + 64);
 
     const int tid = threadIdx.x;
     const long long n_chunks = (S_out + CS - 1) / CS;
@@ -141,8 +165,8 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
 
     for (int i = tid; i < N - 1; i += Cfg::NT)
         tw[i] = tw_g[i];
-    if (tid < NS)
-        mbar_init(full + tid, 1);
+    if (tid < NS + Cfg::FG * Cfg::NSLOT)
+        mbar_init(full + tid, 1); // input ring chunks, then the FFT groups' slots
     fence_mbar_init();
     __syncthreads();
 
@@ -150,34 +174,90 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
         // ================================ FFT role ================================
         if constexpr (Cfg::FFT_REGS < Cfg::LAUNCH_REGS)
             asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(Cfg::FFT_REGS));
-        constexpr int FG = Cfg::FG, FNT = Cfg::FNT;
+        constexpr int FG = Cfg::FG, FNT = Cfg::FNT, NSLOT = Cfg::NSLOT;
+        using S0 = FftSchedule<L, Cfg::W>;
+        constexpr int W0 = S0::width(0), LO0 = S0::lo(0), E0 = 1 << W0, U0 = N >> W0;
         const int fg = (tid - NFIR) / FNT;         // FFT group
         const int ftid = tid - NFIR - fg * FNT;
         const int BAR_FFT = 2 + fg;                // named barrier of the group
-        float2* gtile = tile + fg * (Cfg::TILE_BYTES / sizeof(float2));
+        float2* slots = tile + fg * NSLOT * (Cfg::TILE_BYTES / sizeof(float2));
+        uint64_t* sfull = full + NS + fg * NSLOT;  // per-slot "rows landed" mbarriers
         const long long n_tiles = n_chunks * TPC;
-        // this CTA's tiles blockIdx.x + m * grid, m = fg, fg + FG, ...
-        for (long long j = blockIdx.x + fg * grid; j < n_tiles; j += FG * grid) {
+        // this group's tiles: blockIdx.x + m * grid, m = fg, fg + FG, ... -> i-th tile
+        const long long first = blockIdx.x + fg * grid, stride = FG * grid;
+        const long long my_tiles = n_tiles > first ? (n_tiles - first + stride - 1) / stride : 0;
+        // leader: wait until the tile's chunk is published, then copy its rows
+        // from the ring into the slot (TMA bulk copies: they read L2, so no
+        // stale L1 line can be seen; the proxy fence orders the acquired
+        // generic-proxy data before the async-proxy reads)
+        auto fetch = [&](long long i) {
+            const long long j = first + i * stride;
             const long long k = j / TPC;
-            const int slot = static_cast<int>(k % NSR);
+            const int rslot = static_cast<int>(k % NSR);
             const unsigned epoch = static_cast<unsigned>(k / NSR);
-            if (ftid == 0) // chunk k published: every FIR warp of its C/32 items
-                spin_until_geq(produced + slot, (epoch + 1) * NCB * Cfg::NWF);
-            named_sync(BAR_FFT, FNT);
-            const long long row0 = k * CS + (j - k * TPC) * BT;
-            // ring row (slot, r) == gin + (k*CS + r) * N
-            const float2* gin = ring + slot * Cfg::RING_SLOT_FLOATS2 - k * CS * static_cast<long long>(N);
-#if PPFG_L2X_DEBUG != 2
-            FftPasses<L, L, Cfg::W, true, true, FNT>::run(gin, out, gtile, Cfg::STRIDE, BT,
-                                                         L2xRows{row0, S_out}, tw, ftid,
-                                                         SyncNamed{BAR_FFT, FNT});
-#endif
-            // every thread's ring loads completed in the first pass (before
-            // its barrier); release the tile's rows and the smem tile
-            named_sync(BAR_FFT, FNT);
-            if (ftid == 0) // relaxed: the loads it vouches for have returned their values
-                asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(consumed + slot), "r"(BT)
+            const int s = static_cast<int>(i % NSLOT);
+            spin_until_geq(produced + rslot, (epoch + 1) * NCB * Cfg::NWF);
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            const long long r0 = (j - k * TPC) * BT; // row of the tile in its chunk
+            mbar_arrive_expect_tx(sfull + s, static_cast<uint32_t>(sizeof(float2) * BT * N));
+            const float2* src = ring + rslot * Cfg::RING_SLOT_FLOATS2 + r0 * N;
+            float2* dst = slots + s * (Cfg::TILE_BYTES / sizeof(float2));
+            for (int r = 0; r < BT; ++r)
+                bulk_g2s(dst + r * Cfg::STRIDE, src + static_cast<long long>(r) * N,
+                         static_cast<uint32_t>(sizeof(float2) * N), sfull + s);
+        };
+        if (ftid == 0)
+            for (long long i = 0; i < NSLOT - 1 && i < my_tiles; ++i)
+                fetch(i);
+        for (long long i = 0; i < my_tiles; ++i) {
+            const long long j = first + i * stride;
+            const long long k = j / TPC;
+            const int rslot = static_cast<int>(k % NSR);
+            const int s = static_cast<int>(i % NSLOT);
+            const int ti = static_cast<int>((j - blockIdx.x) / grid);
+            if (ftid == 0) {
+                L2X_TR(1, 2 * fg, ti);
+                if (i + NSLOT - 1 < my_tiles) // its slot was freed by tile i - 1
+                    fetch(i + NSLOT - 1);
+            }
+            float2* slot = slots + s * (Cfg::TILE_BYTES / sizeof(float2));
+            mbar_wait(sfull + s, static_cast<uint32_t>((i / NSLOT) & 1));
+            if (ftid == 0) {
+                L2X_TR(1, 2 * fg + 1, ti);
+                // the rows are in shared memory: the ring slot may be refilled
+                asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(consumed + rslot), "r"(BT)
                              : "memory");
+            }
+            const long long row0 = k * CS + (j - k * TPC) * BT;
+#if PPFG_L2X_DEBUG != 2
+            // first pass: natural-order rows -> registers (one unit per
+            // thread); after the group barrier, back in place at swizzled
+            // slots (as K2r, fft.cuh)
+            static_assert(BT * U0 == FNT, "one first-pass unit per FFT thread");
+            {
+                const int r = ftid / U0;
+                const unsigned fixed = static_cast<unsigned>(ftid % U0);
+                float2 v[E0];
+                const float2* src = slot + r * Cfg::STRIDE + fixed;
+#pragma unroll
+                for (int e = 0; e < E0; ++e)
+                    v[e] = src[static_cast<unsigned>(e) << LO0];
+                fft_stages<L, LO0, W0, true>(v, fixed, tw);
+                named_sync(BAR_FFT, FNT); // every natural-order read of the slot is done
+                float2* d = slot + r * Cfg::STRIDE + sw(fixed);
+#pragma unroll
+                for (int e = 0; e < E0; ++e)
+                    d[sw(static_cast<unsigned>(e) << LO0)] = v[e];
+            }
+            named_sync(BAR_FFT, FNT);
+            FftPasses<L, L, Cfg::W, false, true, FNT, 1>::run(nullptr, out, slot, Cfg::STRIDE, BT,
+                                                             L2xRows{row0, S_out}, tw, ftid,
+                                                             SyncNamed{BAR_FFT, FNT});
+#endif
+            // every read of the slot is done before its next fill is issued
+            named_sync(BAR_FFT, FNT);
+            if (ftid == 0)
+                L2X_TR(1, 4 + fg, ti);
         }
         return;
     }
@@ -230,9 +310,14 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
             cb_prev = cb;
         }
         // the slot's previous chunk (k - NSR) has been read by every FFT tile
-        if (tid == 0)
+        if (tid == 0) {
+            L2X_TR(0, 0, static_cast<int>(m));
             spin_until_geq(consumed + slot, static_cast<unsigned>(k / NSR) * CS);
+            L2X_TR(0, 1, static_cast<int>(m));
+        }
         named_sync(BAR_FIR, NFIR);
+        if (tid == 0)
+            L2X_TR(0, 2, static_cast<int>(m));
         float2* dst = ring + slot * Cfg::RING_SLOT_FLOATS2 + cb * 32 + lane;
         const long long g0 = m * NIC; // this item's first input chunk
 #pragma unroll 1
@@ -253,8 +338,12 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
             }
 #endif
             const long long need = min(g0 + st + NEED - 1, g0 + NIC - 1);
+            if (tid == 0 && st == 0)
+                L2X_TR(0, 3, static_cast<int>(m));
             for (; waited <= need; ++waited)
                 mbar_wait(full + static_cast<int>(waited % NS), static_cast<uint32_t>((waited / NS) & 1));
+            if (tid == 0 && st == 0)
+                L2X_TR(0, 4, static_cast<int>(m));
             // rows st*RB + warp*U + [0, U + T - 1) of the item's input
             const int r0 = st * RB + warp * U;
             acc_t acc[U];
@@ -301,7 +390,12 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
                     y = make_float2(__double2float_rn(acc[u].x), __double2float_rn(acc[u].y));
                 else
                     y = acc[u];
+#if PPFG_L2X_DEBUG != 3
                 dst[static_cast<size_t>(r0 + u) * N] = y;
+#else
+                if (y.x == 12345.f) // keep the math; skip the ring stores
+                    dst[static_cast<size_t>(r0 + u) * N] = y;
+#endif
             }
         }
         // publish the item per warp: the warp's ring stores, then one
@@ -309,6 +403,8 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
         // NWF * C/32 of them per chunk) — a release waits for the releasing
         // warp's own stores only, so the warps do not serialise on one fence
         __syncwarp();
+        if (tid == 0)
+            L2X_TR(0, 5, static_cast<int>(m));
         if (lane == 0)
             red_release_gpu_add(produced + slot, 1);
         named_sync(BAR_FIR, NFIR); // every warp is done with the item's input chunks

@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <list>
 #include <map>
 #include <mutex>
@@ -716,7 +717,10 @@ bool launch_tiny(ppfg_plan p, const float2* din, uint64_t S_in, float2* dout, cu
 // the plan (counters zeroed per launch; launches sharing them are ordered)
 int launch_l2x(ppfg_plan p, const float2* din, uint64_t S_in, float2* dout, cudaStream_t st) {
     const L2xEntry* e = p->l2x;
-    const size_t ctr_bytes = sizeof(unsigned) * 2 * e->nsr;
+    // counters [2 * nsr], the trace flag, then (at +256 B) the debug timeline
+    const char* trace_path = std::getenv("PPFG_L2X_TRACE");
+    constexpr size_t kTraceBytes = sizeof(unsigned long long) * 2 * 8 * 256;
+    const size_t ctr_bytes = 256 + (trace_path ? kTraceBytes : 0);
     if (p->ring_bytes < e->ring_bytes + ctr_bytes) {
         if (p->d_ring) {
             PPFG_CUDA(cudaStreamSynchronize(st));
@@ -733,6 +737,10 @@ int launch_l2x(ppfg_plan p, const float2* din, uint64_t S_in, float2* dout, cuda
         PPFG_CUDA(cudaStreamWaitEvent(st, p->ev_ring, 0)); // a previous launch on another stream
     unsigned* ctr = reinterpret_cast<unsigned*>(static_cast<char*>(p->d_ring) + e->ring_bytes);
     PPFG_CUDA(cudaMemsetAsync(ctr, 0, ctr_bytes, st));
+    if (trace_path) {
+        static const unsigned one = 1;
+        PPFG_CUDA(cudaMemcpyAsync(ctr + 2 * e->nsr, &one, sizeof(one), cudaMemcpyHostToDevice, st));
+    }
     PPFG_TRY(ensure_smem_attr(e->fn, e->smem, p->device));
     CUtensorMap map;
     PPFG_TRY(encode_rows_map(&map, din, p->C, S_in, 32, e->rb));
@@ -742,6 +750,16 @@ int launch_l2x(ppfg_plan p, const float2* din, uint64_t S_in, float2* dout, cuda
     PPFG_CUDA(cudaLaunchKernel(e->fn, dim3(static_cast<unsigned>(p->num_sms)), dim3(e->nt), args, e->smem, st));
     PPFG_TRY(check_launch("fused fir+fft kernel (L2 exchange)"));
     PPFG_CUDA(cudaEventRecord(p->ev_ring, st));
+    if (trace_path) { // debug: dump CTA 0's timeline (u64 [2][8][256], ns)
+        std::vector<unsigned long long> tr(2 * 8 * 256);
+        PPFG_CUDA(cudaMemcpyAsync(tr.data(), reinterpret_cast<char*>(ctr) + 256, kTraceBytes,
+                                  cudaMemcpyDeviceToHost, st));
+        PPFG_CUDA(cudaStreamSynchronize(st));
+        if (FILE* f = std::fopen(trace_path, "wb")) {
+            std::fwrite(tr.data(), 1, kTraceBytes, f);
+            std::fclose(f);
+        }
+    }
     return PPFG_OK;
 }
 
