@@ -18,7 +18,9 @@ std::vector<FusedEntry> fused_part_main() {
     // EXACT C=512 T=8 0.68 -> 0.77, EXACT C=256 T=16 0.53 -> 0.56, C=256 T=32
     // 0.605 -> 0.635. Not on the T = 1 FFT entries (C=256 0.90 -> 0.85,
     // C=1024 0.884 -> 0.868) nor TRIV there (channelize_block must stay
-    // bit-exact). With several FIR groups per CTA (C <= 512 at R = 4,
+    // bit-exact). With HS the SKA entry no longer gains from the L2 prefetch
+    // one chunk ahead (L2A): 6.5 GB bench 3236-3242 with it, 3279-3283
+    // without, 3105-3108 two chunks ahead. With several FIR groups per CTA (C <= 512 at R = 4,
     // C <= 256 at R = 2) HS helped every EXACT shape (C=128 T=8 0.71 -> 0.75,
     // C=256 0.756 -> 0.769, C=512 T=4 0.85 -> 0.90), FAST at T >= 16 (C=256
     // T=16 0.84 -> 0.86, C=128 T=32 0.626 -> 0.644), C=64 T=8 (0.88 -> 0.92)
@@ -35,7 +37,7 @@ std::vector<FusedEntry> fused_part_main() {
         // 0.90 — but not at C=1024 T=4: 0.83 vs 0.86; FIR/FFT registers
         // 136/120 instead of 160/96 at C=512 T=16 0.76 vs 0.72 and FP64
         // C=1024 T=4 0.762 vs 0.753)
-        fused_entry<FusedCfg<10, 8, 2, false, 120, 80, 2, 3, 2, true, 1, true, true>>(),
+        fused_entry<FusedCfg<10, 8, 2, false, 120, 80, 2, 3, 2, true, 0, true, true>>(),
         fused_entry<FusedCfg<9, 8, 2, false, 120, 80, 2, 3>>(),
         fused_entry<FusedCfg<8, 8, 2, false, 120, 80, 2, 3>>(),
         fused_entry<FusedCfg<7, 8, 2, false, 120, 80, 2, 3>>(),
