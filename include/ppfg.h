@@ -150,7 +150,7 @@ int ppfg_fir_fft_mean_power(ppfg_plan plan, const void* in, uint64_t n_spectra_i
 
 /* Which kernel ppfg_fir_fft will run for this plan: 0 = unfused FIR+FFT,
  * 1 = fused FP32-FIR, 2 = fused FP64 (bit-exact) FIR, 3 / 4 = the cluster
- * versions of 1 / 2, 5 / 6 = the warp-level tiny-C (2..32) versions of 1 / 2,
+ * versions of 1 / 2, 5 / 6 = the warp-level tiny-C (1..32) versions of 1 / 2,
  * 7 / 8 = the L2-exchange versions (K7) of 1 / 2. */
 int ppfg_fir_fft_kind(ppfg_plan plan);
 /* The kernel ppfg_fir_fft launches for this plan, named the way ncu prints it

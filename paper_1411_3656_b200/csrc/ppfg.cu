@@ -683,18 +683,22 @@ bool launch_fir_fast(ppfg_plan p, const float2* din, uint64_t S_in, float2* dout
 // takes the plain-load kernels instead
 bool aligned16(const void* ptr) { return reinterpret_cast<uintptr_t>(ptr) % 16 == 0; }
 
-// K6: tiny power-of-two C (2..32), one warp-level kernel (tiny.cuh). Lane
+bool tiny_exact(ppfg_plan p) { return !(p->flags & PPFG_FAST) || p->L == 0; }
+
+// K6: tiny power-of-two C (1..32), one warp-level kernel (tiny.cuh). Lane
 // groups of C lanes take contiguous time segments (a multiple of T spectra,
 // enough segments for ~4 waves of 48 warps per SM).
 bool launch_tiny(ppfg_plan p, const float2* din, uint64_t S_in, float2* dout, cudaStream_t st, int* rc) {
-    if (p->L < 1 || p->L > 5 || (p->flags & PPFG_UNFUSED))
+    if (p->L < 0 || p->L > 5 || (p->flags & PPFG_UNFUSED))
         return false;
-    const KernelFn fn = tiny_table(p->L, static_cast<int>(p->T), !(p->flags & PPFG_FAST));
+    // C = 1 is the FIR alone, whose north-star bar (1e-6) an FP32 chain misses
+    // at T >= 16: it always takes the FP64 (bit-exact) variant
+    const KernelFn fn = tiny_table(p->L, static_cast<int>(p->T), tiny_exact(p));
     if (!fn)
         return false;
     const uint64_t T = p->T, S_out = S_in - T + 1;
     // tiny.cuh: the step loop's unroll max(T, PF) (segments are whole unrolls)
-    const bool pf16 = T == 16 || (T == 8 && (!(p->flags & PPFG_FAST) || p->L <= 3));
+    const bool pf16 = T == 16 || (T == 8 && (tiny_exact(p) || p->L <= 3));
     const uint64_t unroll = std::max<uint64_t>(T, pf16 ? 16 : 8);
     const uint64_t groups_per_warp = 32 >> p->L;
     const uint64_t target = static_cast<uint64_t>(p->num_sms) * 48 * 4 * groups_per_warp;
@@ -1416,9 +1420,9 @@ void* ppfg_plan_stream(ppfg_plan plan) { return plan ? plan->stream : nullptr; }
 const char* ppfg_fir_fft_kernel_name(ppfg_plan p) {
     if (!p)
         return "";
-    if (!(p->flags & PPFG_UNFUSED) && p->L >= 1 && p->L <= 5 && p->T > 0 &&
-        tiny_table(p->L, static_cast<int>(p->T), !(p->flags & PPFG_FAST)))
-        return p->flags & PPFG_FAST ? "fused_tiny_kernel (FP32 FIR)" : "fused_tiny_kernel (FP64 FIR)";
+    if (!(p->flags & PPFG_UNFUSED) && p->L >= 0 && p->L <= 5 && p->T > 0 &&
+        tiny_table(p->L, static_cast<int>(p->T), tiny_exact(p)))
+        return tiny_exact(p) ? "fused_tiny_kernel (FP64 FIR)" : "fused_tiny_kernel (FP32 FIR)";
     if (!(p->l2x || p->fused) || (p->flags & PPFG_UNFUSED))
         return "unfused (FIR kernel + FFT kernel)";
     return p->fused_name.c_str();
@@ -1458,9 +1462,9 @@ int ppfg_device_hbm_gbs(int device, double* gbs) {
 }
 
 int ppfg_fir_fft_kind(ppfg_plan p) {
-    if (p && !(p->flags & PPFG_UNFUSED) && p->L >= 1 && p->L <= 5 && p->T > 0 &&
-        tiny_table(p->L, static_cast<int>(p->T), !(p->flags & PPFG_FAST)))
-        return p->flags & PPFG_FAST ? 5 : 6;
+    if (p && !(p->flags & PPFG_UNFUSED) && p->L >= 0 && p->L <= 5 && p->T > 0 &&
+        tiny_table(p->L, static_cast<int>(p->T), tiny_exact(p)))
+        return tiny_exact(p) ? 6 : 5;
     if (p && p->l2x && !(p->flags & PPFG_UNFUSED))
         return p->l2x->exact ? 8 : 7;
     if (!p || !p->fused || (p->flags & PPFG_UNFUSED))

@@ -1,5 +1,5 @@
 // tab_tiny.cu — K6 fused FIR + FFT for tiny power-of-two C (tiny.cuh):
-// C = 2..32 at the acceptance tap counts T = 1, 2, 4, 8, 16 (FP32 and FP64
+// C = 1..32 at the acceptance tap counts T = 1, 2, 4, 8, 16 (FP32 and FP64
 // FIR) and T = 32 (FP32; the FP64 window would not fit the registers).
 #include "tables_impl.cuh"
 
@@ -27,6 +27,7 @@ KernelFn tiny_t(int T, bool exact) {
 
 KernelFn tiny_table(int L, int T, bool exact) {
     switch (L) {
+    case 0: return tiny_t<0>(T, exact);
     case 1: return tiny_t<1>(T, exact);
     case 2: return tiny_t<2>(T, exact);
     case 3: return tiny_t<3>(T, exact);

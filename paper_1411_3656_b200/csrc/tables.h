@@ -88,7 +88,7 @@ struct L2xEntry {
 };
 std::vector<L2xEntry> l2x_table(); // tab_l2x.cu
 
-// K6 fused FIR+FFT for C = 2^L, L = 1..5 (tiny.cuh), tab_tiny.cu; nullptr
+// K6 fused FIR+FFT for C = 2^L, L = 0..5 (tiny.cuh), tab_tiny.cu; nullptr
 // where no instantiation covers (L, T, exact)
 KernelFn tiny_table(int L, int T, bool exact);
 

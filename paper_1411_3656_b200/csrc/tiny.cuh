@@ -1,6 +1,7 @@
 // tiny.cuh — K6: fused FIR + C-point FFT for small power-of-two channel
-// counts (C = 2..32, SURVEY §8f row 2 "tiny C"), one warp-level kernel with
-// no HBM round trip for the filtered block and no shared memory.
+// counts (C = 1..32, SURVEY §8f row 2 "tiny C"), one warp-level kernel with
+// no HBM round trip for the filtered block and no shared memory (C = 1: 32
+// single-lane groups per warp, the 1-point FFT being the identity).
 //
 // A warp holds 32 / C lane groups; lane c of a group owns channel c of a
 // contiguous time segment of output spectra. Per output spectrum the lane
@@ -36,7 +37,7 @@ __global__ void __launch_bounds__(256) fused_tiny_kernel(const float2* __restric
                                                          long long n_tasks) {
     constexpr int N = 1 << L;   // channels (lanes per group)
     constexpr int G = 32 / N;   // groups (time segments) per warp
-    static_assert(L >= 1 && L <= 5, "C = 2..32");
+    static_assert(L >= 0 && L <= 5, "C = 1..32 (C = 1: the 1-point FFT is the identity)");
     using Acc = typename std::conditional<EXACT, double, float>::type;
     const int lane = threadIdx.x & 31;
     const int q = lane >> L;
@@ -55,7 +56,7 @@ __global__ void __launch_bounds__(256) fused_tiny_kernel(const float2* __restric
         h[t] = static_cast<Acc>(__ldg(taps + t * N + c));
     // this lane's twiddle per stage (the pair's shared tw[h-1+j], j from the
     // label bits above the stage's bit)
-    float2 w[L];
+    float2 w[L > 0 ? L : 1];
 #pragma unroll
     for (int s = 1; s <= L; ++s) {
         const int b = L - s;
