@@ -697,6 +697,20 @@ bool launch_tiny(ppfg_plan p, const float2* din, uint64_t S_in, float2* dout, cu
     if (!fn)
         return false;
     const uint64_t T = p->T, S_out = S_in - T + 1;
+    if (p->L == 0) { // fir_c1_kernel: one warp per segment of whole 32-spectrum steps
+        const uint64_t target = static_cast<uint64_t>(p->num_sms) * 48 * 4;
+        uint64_t seg = std::max<uint64_t>(cdiv(S_out, target), 32);
+        seg = cdiv(seg, 32) * 32;
+        long long n_tasks = static_cast<long long>(cdiv(S_out, seg));
+        long long S_in_ll = static_cast<long long>(S_in), S_out_ll = static_cast<long long>(S_out);
+        int seg_i = static_cast<int>(seg);
+        void* args[] = {&din, &dout, &S_in_ll, &S_out_ll, &p->d_taps, &seg_i, &n_tasks};
+        *rc = cudaLaunchKernel(fn, dim3(static_cast<unsigned>(cdiv(static_cast<uint64_t>(n_tasks) * 32, 256))),
+                               dim3(256), args, 0, st) == cudaSuccess
+                  ? check_launch("fir kernel (C = 1)")
+                  : fail(PPFG_CUDA_ERROR, "fir kernel (C = 1): launch failed");
+        return true;
+    }
     // tiny.cuh: the step loop's unroll max(T, PF) (segments are whole unrolls)
     const bool pf16 = T == 16 || (T == 8 && (tiny_exact(p) || p->L <= 3));
     const uint64_t unroll = std::max<uint64_t>(T, pf16 ? 16 : 8);

@@ -25,9 +25,21 @@ KernelFn tiny_t(int T, bool exact) {
 }
 } // namespace
 
+KernelFn fir_c1_table(int T) {
+    switch (T) {
+    case 1: return reinterpret_cast<KernelFn>(&fir_c1_kernel<1>);
+    case 2: return reinterpret_cast<KernelFn>(&fir_c1_kernel<2>);
+    case 4: return reinterpret_cast<KernelFn>(&fir_c1_kernel<4>);
+    case 8: return reinterpret_cast<KernelFn>(&fir_c1_kernel<8>);
+    case 16: return reinterpret_cast<KernelFn>(&fir_c1_kernel<16>);
+    case 32: return reinterpret_cast<KernelFn>(&fir_c1_kernel<32>);
+    default: return nullptr;
+    }
+}
+
 KernelFn tiny_table(int L, int T, bool exact) {
     switch (L) {
-    case 0: return tiny_t<0>(T, exact);
+    case 0: return exact ? fir_c1_table(T) : nullptr; // C = 1: the coalesced FP64 FIR kernel
     case 1: return tiny_t<1>(T, exact);
     case 2: return tiny_t<2>(T, exact);
     case 3: return tiny_t<3>(T, exact);

@@ -91,5 +91,6 @@ std::vector<L2xEntry> l2x_table(); // tab_l2x.cu
 // K6 fused FIR+FFT for C = 2^L, L = 0..5 (tiny.cuh), tab_tiny.cu; nullptr
 // where no instantiation covers (L, T, exact)
 KernelFn tiny_table(int L, int T, bool exact);
+KernelFn fir_c1_table(int T); // K6 at C = 1 (fir_c1_kernel), tab_tiny.cu
 
 } // namespace ppfg
