@@ -145,7 +145,8 @@ namespace ppfg {
 // CONSECUTIVE output spectra instead of separate segments, so every load and
 // store of a warp is one contiguous 256-byte run. Each warp walks its segment
 // 32 spectra per step: it loads the next 32 input samples (coalesced) into a
-// per-warp ring of 3 x 32 samples in shared memory, and lane l filters
+// per-warp ring of 3 x 32 samples in shared memory (converted to double once
+// on arrival), and lane l filters
 // y[s0 + l] = sum_t h[t] x[s0 + l + t] from the ring (consecutive lanes read
 // consecutive samples: conflict-free), in FP64 in ascending tap order from
 // h0*x0 — bit-identical to ppf_fir_optimized (fir.hpp:85-110). T <= 33.
@@ -155,12 +156,12 @@ __global__ void __launch_bounds__(256) fir_c1_kernel(const float2* __restrict__ 
                                                      long long S_out, const float* __restrict__ taps,
                                                      int seg, long long n_tasks) {
     static_assert(T >= 1 && T <= 33, "a window spans at most two 32-sample chunks");
-    __shared__ float2 ring_s[8][96];
+    __shared__ double2 ring_s[8][96]; // converted once on arrival, read T times
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const long long task = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     if (task >= n_tasks)
         return;
-    float2* ring = ring_s[wib];
+    double2* ring = ring_s[wib];
     const long long s0 = task * seg;
     const long long s1 = min(s0 + seg, S_out);
     double h[T];
@@ -168,9 +169,10 @@ __global__ void __launch_bounds__(256) fir_c1_kernel(const float2* __restrict__ 
     for (int t = 0; t < T; ++t)
         h[t] = static_cast<double>(__ldg(taps + t));
     auto ld = [&](long long i) { return i < S_in ? __ldcs(in + i) : make_float2(0.f, 0.f); };
+    auto cvt = [](float2 v) { return make_double2(static_cast<double>(v.x), static_cast<double>(v.y)); };
     // chunk q (samples s0 + 32q ..) lives in ring slot q % 3
-    ring[lane] = ld(s0 + lane);
-    ring[32 + lane] = ld(s0 + 32 + lane);
+    ring[lane] = cvt(ld(s0 + lane));
+    ring[32 + lane] = cvt(ld(s0 + 32 + lane));
     float2 next = ld(s0 + 64 + lane);
     int q = 0;
     for (long long s = s0; s < s1; s += 32, ++q) {
@@ -179,19 +181,19 @@ __global__ void __launch_bounds__(256) fir_c1_kernel(const float2* __restrict__ 
 #pragma unroll
         for (int t = 0; t < T; ++t) {
             const int i = lane + t; // chunk q (i < 32) or q + 1
-            const float2 x = ring[((q + (i >> 5)) % 3) * 32 + (i & 31)];
+            const double2 x = ring[((q + (i >> 5)) % 3) * 32 + (i & 31)];
             if (t == 0) {
-                ar = __dmul_rn(h[0], static_cast<double>(x.x));
-                ai = __dmul_rn(h[0], static_cast<double>(x.y));
+                ar = __dmul_rn(h[0], x.x);
+                ai = __dmul_rn(h[0], x.y);
             } else {
-                ar = __fma_rn(h[t], static_cast<double>(x.x), ar);
-                ai = __fma_rn(h[t], static_cast<double>(x.y), ai);
+                ar = __fma_rn(h[t], x.x, ar);
+                ai = __fma_rn(h[t], x.y, ai);
             }
         }
         if (s + lane < s1)
             __stcs(out + s + lane, make_float2(__double2float_rn(ar), __double2float_rn(ai)));
         __syncwarp();
-        ring[((q + 2) % 3) * 32 + lane] = next; // chunk q + 2 replaces chunk q
+        ring[((q + 2) % 3) * 32 + lane] = cvt(next); // chunk q + 2 replaces chunk q - 1
         next = ld(s + 96 + lane);
     }
 }
