@@ -26,7 +26,9 @@ std::vector<FusedEntry> fused_part_main() {
     // T=16 0.84 -> 0.86, C=128 T=32 0.626 -> 0.644), C=64 T=8 (0.88 -> 0.92)
     // and C=256 T=4 (0.794 -> 0.81), but not FAST C=128..512 at T=8 (cfg1
     // C=512: 0.90 -> 0.82) nor C=512 T=4 (0.89 -> 0.85): those keep
-    // whole-tile handoff.
+    // whole-tile handoff. Fewer channels per FIR thread (RLOG) make one FIR
+    // group per CTA, where HS applies: C=512 T=8 (cfg1) R=2 + HS 0.90 -> 0.94,
+    // C=256 T=8 R=1 + HS 0.82 -> 0.92 (R = 2 without HS: 0.89-0.925).
     return {
         // (float4 twiddle tables where they measured faster than float2:
         // C=1024 T=8 FAST 0.86 vs 0.85 at the SKA size, C=512 EXACT 0.68 vs
@@ -38,8 +40,8 @@ std::vector<FusedEntry> fused_part_main() {
         // 136/120 instead of 160/96 at C=512 T=16 0.76 vs 0.72 and FP64
         // C=1024 T=4 0.762 vs 0.753)
         fused_entry<FusedCfg<10, 8, 2, false, 120, 80, 2, 3, 2, true, 0, true, true>>(),
-        fused_entry<FusedCfg<9, 8, 2, false, 120, 80, 2, 3>>(),
-        fused_entry<FusedCfg<8, 8, 2, false, 120, 80, 2, 3>>(),
+        fused_entry<FusedCfg<9, 8, 1, false, 120, 80, 2, 3, 2, false, 0, true>>(),
+        fused_entry<FusedCfg<8, 8, 0, false, 120, 80, 2, 3, 2, false, 0, true>>(),
         fused_entry<FusedCfg<7, 8, 2, false, 120, 80, 2, 3>>(),
         fused_entry<FusedCfg<6, 8, 1, false, 120, 80, 2, 3, 2, true, 0, true>>(),
         fused_entry<FusedCfg<10, 4, 2, false, 160, 96, 4, 2, 2, false, 0, true, true>>(),
