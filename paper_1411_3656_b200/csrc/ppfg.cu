@@ -217,6 +217,7 @@ struct ppfg_plan_s {
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     const FusedEntry* fused = nullptr;
+    const FusedEntry* fused_power = nullptr; // detection-only configuration, if any
     std::string fused_name; // the fused kernel's configuration, as ncu prints it
     // K7 (l2x.cuh): the exchange ring + its counters (grow-only) and an event
     // ordering launches that share them
@@ -840,7 +841,7 @@ int launch_mean_power(ppfg_plan p, const float2* bins, uint64_t n, double* dmean
 int launch_fir_fft_mean_power(ppfg_plan p, const float2* din, uint64_t S_in, double* dmean,
                               cudaStream_t st) {
     const uint64_t S_out = S_in - p->T + 1;
-    const FusedEntry* e = p->fused;
+    const FusedEntry* e = p->fused_power && p->fused ? p->fused_power : p->fused;
     if (e && e->power_fn && !(p->flags & PPFG_UNFUSED) && aligned16(din)) {
         // partials: at most one CTA per SM, power_rows rows of C doubles each
         PPFG_TRY(ensure_parts(p, static_cast<size_t>(p->num_sms) * e->power_rows * p->C * sizeof(double)));
@@ -1339,7 +1340,7 @@ int ppfg_plan_create(ppfg_plan* plan, uint64_t n_channels, uint64_t n_taps,
     }
     if (p->L >= 0) {
         for (const auto& e : fused_table()) {
-            if (e.L == p->L && e.T == 1 && e.q == 1) {
+            if (!e.power_only && e.L == p->L && e.T == 1 && e.q == 1) {
                 std::vector<float> ones(n_channels, 1.0f);
                 if (cudaMalloc(&p->d_ones, n_channels * sizeof(float)) != cudaSuccess ||
                     cudaMemcpy(p->d_ones, ones.data(), n_channels * sizeof(float),
@@ -1367,7 +1368,12 @@ int ppfg_plan_create(ppfg_plan* plan, uint64_t n_channels, uint64_t n_taps,
         // FIR -> HBM -> FFT; PPFG_CLUSTER forces them.
         const bool want_cluster = (flags & PPFG_CLUSTER) != 0;
         for (const auto& e : fused_table()) {
-            if (e.L == p->L && e.T == static_cast<int>(n_taps) && e.exact == exact &&
+            if (e.power_only && !p->fused_power && e.L == p->L && e.T == static_cast<int>(n_taps) &&
+                e.exact == exact)
+                p->fused_power = &e;
+        }
+        for (const auto& e : fused_table()) {
+            if (!e.power_only && e.L == p->L && e.T == static_cast<int>(n_taps) && e.exact == exact &&
                 (e.q == 1 || want_cluster || e.preferred)) {
                 p->fused = &e;
                 p->fused_name = kernel_name_of(e);

@@ -44,6 +44,9 @@ std::vector<FusedEntry> fused_part_main() {
         // 136/120 instead of 160/96 at C=512 T=16 0.76 vs 0.72 and FP64
         // C=1024 T=4 0.762 vs 0.753)
         fused_entry<FusedCfg<10, 8, 2, false, 120, 80, 2, 3, 2, true, 0, true, true>>(),
+        // detection (mean power) at the SKA shape: two FFT warpgroups with 96
+        // registers hold the per-bin accumulators next to the pass values
+        power_entry<FusedCfg<10, 8, 2, false, 160, 96, 2, 2, 2, true, 0, true, true>>(),
         fused_entry<FusedCfg<9, 8, 1, false, 120, 80, 2, 3, 2, false, 0, true>>(),
         fused_entry<FusedCfg<8, 8, 0, false, 120, 80, 2, 3, 2, false, 0, true>>(),
         fused_entry<FusedCfg<7, 8, 1, false, 120, 80, 2, 3, 2, false, 0, true>>(),

@@ -26,6 +26,7 @@ struct FusedEntry {
     int power_rows = 0;          // its partials per CTA (tile rows)
     bool tw4 = false;            // takes the pre-expanded float4 twiddle table
     const char* sig = nullptr;   // __PRETTY_FUNCTION__ of the entry maker: names the Cfg
+    bool power_only = false;     // a detection-only configuration (power_fn; fn unused)
 };
 
 struct FftEntry {

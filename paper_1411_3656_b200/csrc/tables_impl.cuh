@@ -34,6 +34,16 @@ FusedEntry fused_entry() {
     return e;
 }
 
+// A configuration used for detection only (fir_fft_mean_power): its register
+// split / FFT warpgroups are chosen for the accumulating last pass
+template <class Cfg>
+FusedEntry power_entry() {
+    static_assert(has_power<Cfg>(), "detection variant");
+    FusedEntry e = fused_entry<Cfg>();
+    e.power_only = true;
+    return e;
+}
+
 template <class Cfg>
 FusedEntry split_entry(bool preferred) {
     FusedEntry e{Cfg::L,    Cfg::T,  Cfg::EXACT, reinterpret_cast<KernelFn>(&fused_split_kernel<Cfg>),
