@@ -38,6 +38,7 @@
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <sys/mman.h>
 #include <utility>
 #include <vector>
 
@@ -303,6 +304,23 @@ private:
 };
 
 namespace detail {
+// Large result vectors are freshly allocated on every call (the reference API
+// returns them by value); above glibc's mmap threshold each call page-faults
+// them in 4 KB at a time. Ask for transparent huge pages on the vector's
+// storage before its first touch (a hint: no effect where THP is disabled).
+template <class T>
+inline void reserve_huge(std::vector<T>& v, std::size_t n) {
+    v.reserve(n);
+    constexpr std::uintptr_t kHuge = std::uintptr_t(2) << 20;
+    const std::size_t bytes = n * sizeof(T);
+    if (bytes < 2 * kHuge)
+        return;
+    const std::uintptr_t b = reinterpret_cast<std::uintptr_t>(v.data());
+    const std::uintptr_t lo = (b + kHuge - 1) & ~(kHuge - 1), hi = (b + bytes) & ~(kHuge - 1);
+    if (hi > lo)
+        ::madvise(reinterpret_cast<void*>(lo), hi - lo, MADV_HUGEPAGE);
+}
+
 // Process-wide cache of device plans for the one-shot calls (ppf_fir_*,
 // channelize_block): the reference API is stateless and a caller looping per
 // block (bench.hpp:129-150, pipeline.hpp:121-136) would otherwise pay plan
@@ -396,6 +414,7 @@ inline FilteredBlock run_fir(const SampleBlock& input, const FilterCoefficients&
     FilteredBlock out;
     out.n_channels = input.n_channels;
     out.n_spectra_out = input.n_spectra() - coeffs.n_taps + 1;
+    detail::reserve_huge(out.spectra, out.n_spectra_out * out.n_channels);
     out.spectra.resize(out.n_spectra_out * out.n_channels);
     auto p = PlanCache::instance().acquire(coeffs.n_channels, coeffs.n_taps, coeffs.values.data());
     auto fn = reference_order ? ppfg_fir_reference_order : ppfg_fir;
@@ -483,6 +502,7 @@ inline ChannelizedOutput channelize_block(const FilteredBlock& filtered, bool ff
     if (!is_power_of_two(out.n_channels) && !fft_fallback)
         throw unsupported_size_error(
             "channelize_block: non-power-of-two channel count with fallback disabled");
+    detail::reserve_huge(out.bins, filtered.spectra.size());
     out.bins.resize(filtered.spectra.size());
     auto p = detail::PlanCache::instance().acquire(filtered.n_channels, 0, nullptr);
     detail::check(ppfg_channelize(p.get(), filtered.spectra.data(), out.n_spectra, out.bins.data(),
@@ -530,7 +550,7 @@ inline SampleBlock carry_history(StreamState& state, const SampleBlock& block, s
     const std::size_t nc = block.n_channels;
     SampleBlock joined;
     joined.n_channels = nc;
-    joined.samples.reserve(state.history.size() + block.samples.size());
+    detail::reserve_huge(joined.samples, state.history.size() + block.samples.size());
     joined.samples.insert(joined.samples.end(), state.history.begin(), state.history.end());
     joined.samples.insert(joined.samples.end(), block.samples.begin(), block.samples.end());
     const std::size_t avail = joined.samples.size() / (nc ? nc : 1);
