@@ -51,8 +51,11 @@ constexpr int ilcm(int a, int b) {
 
 template <int L_, int T_, int RLOG_, bool EXACT_, int FIR_REGS_ = 160, int FFT_REGS_ = 96,
           int PC_ = 4, int FFT_WG_ = 2, int NTILE_ = 2, bool TW4_ = false, int L2A_ = 0,
-          bool HS_ = false, bool TRIV_ = false>
+          bool HS_ = false, bool TRIV_ = false, bool PAIR_ = false>
 struct FusedCfg {
+    // PAIR: two consecutive spectra per FIR step with interleaved accumulation
+    // chains (same per-output operation order; fused_split.cuh SplitCfg::PAIR)
+    static constexpr bool PAIR = PAIR_;
     // HS: hand tiles over per FFT pass group instead of whole: a FIR thread
     // arrives on FULL[t][pg] as soon as it has written its rows of pass group
     // pg and waits on EMPTY[t][pg] just before writing them, so each FFT
@@ -124,6 +127,8 @@ struct FusedCfg {
     static_assert(!HS || FFT_SPLIT, "per-pass-group handoff needs an evenly split tile");
     static_assert(!HS || 1 + 2 * NTILE * PGROUPS + PGROUPS <= 16, "named barriers");
     static_assert(!TRIV || (!EXACT && RLOG == 2), "trivial prestages: FAST, R = 4");
+    static_assert(!PAIR || (B % 2 == 0 && T >= 2 && (!HS || PROWS % 2 == 0)),
+                  "spectrum pairs within a batch and a pass group");
     // named barrier ids (0 = __syncthreads): FULL[t][pg], EMPTY[t][pg], pass
     // syncs per pass group (HS: per pass group; else one FULL / EMPTY per tile)
     static constexpr int HPG = HS ? PGROUPS : 1;          // handoff groups per tile
@@ -364,50 +369,122 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
             // Rows past the group's end (partial or absent chunk) read stale
             // ring data: they only feed outputs the FFT role never stores, and
             // keeping the loads unpredicated lets the window rotate by renaming.
+            if constexpr (Cfg::PAIR) {
 #pragma unroll
-            for (int i = 0; i < B; ++i) {
-                if constexpr (Cfg::HS) { // tile row g*B+i's pass group has drained tile t
-                    const int r = g * B + i;
-                    if ((i == 0 || r % Cfg::PROWS == 0) && b >= Cfg::NTILE)
-                        named_sync(Cfg::bar_empty(t, r / Cfg::PROWS), Cfg::hcount(r / Cfg::PROWS));
-                }
-                float2 y[R];
+                for (int i = 0; i < B; i += 2) {
+                    if constexpr (Cfg::HS) { // tile rows g*B+i, +1: their pass group has drained tile t
+                        const int r = g * B + i;
+                        if ((i == 0 || r % Cfg::PROWS == 0) && b >= Cfg::NTILE)
+                            named_sync(Cfg::bar_empty(t, r / Cfg::PROWS), Cfg::hcount(r / Cfg::PROWS));
+                    }
+                    float2 y0[R], y1[R];
 #pragma unroll
-                for (int k = 0; k < R; ++k) {
-                    const float2 x = chunk[i * N + k * NTG];
+                    for (int k = 0; k < R; ++k) {
+                        // window: xw[k][t] = x[i + t - 1], t = 1..T-1; output i reads
+                        // (xw[1..T-1], a), output i+1 (xw[2..T-1], a, b)
+                        const float2 xa = chunk[i * N + k * NTG], xb = chunk[(i + 1) * N + k * NTG];
+                        Win a, bb;
+                        a.x = static_cast<Acc>(xa.x);
+                        a.y = static_cast<Acc>(xa.y);
+                        bb.x = static_cast<Acc>(xb.x);
+                        bb.y = static_cast<Acc>(xb.y);
+                        auto v0 = [&](int tt) -> Win { return tt + 1 <= T - 1 ? xw[k][tt + 1] : a; };
+                        auto v1 = [&](int tt) -> Win {
+                            return tt + 2 <= T - 1 ? xw[k][tt + 2] : (tt + 2 == T ? a : bb);
+                        };
+                        if constexpr (Cfg::EXACT) {
+                            double ar0 = __dmul_rn(h[k][0], v0(0).x), ai0 = __dmul_rn(h[k][0], v0(0).y);
+                            double ar1 = __dmul_rn(h[k][0], v1(0).x), ai1 = __dmul_rn(h[k][0], v1(0).y);
 #pragma unroll
-                    for (int tt = 0; tt + 1 < T; ++tt)
-                        xw[k][tt] = xw[k][tt + 1];
-                    xw[k][T - 1].x = static_cast<Acc>(x.x);
-                    xw[k][T - 1].y = static_cast<Acc>(x.y);
-                    if constexpr (Cfg::EXACT) {
-                        double ar = __dmul_rn(h[k][0], xw[k][0].x);
-                        double ai = __dmul_rn(h[k][0], xw[k][0].y);
+                            for (int tt = 1; tt < T; ++tt) {
+                                ar0 = __fma_rn(h[k][tt], v0(tt).x, ar0);
+                                ai0 = __fma_rn(h[k][tt], v0(tt).y, ai0);
+                                ar1 = __fma_rn(h[k][tt], v1(tt).x, ar1);
+                                ai1 = __fma_rn(h[k][tt], v1(tt).y, ai1);
+                            }
+                            y0[k] = make_float2(__double2float_rn(ar0), __double2float_rn(ai0));
+                            y1[k] = make_float2(__double2float_rn(ar1), __double2float_rn(ai1));
+                        } else {
+                            float2 acc0 = mul2s(h[k][0], v0(0)), acc1 = mul2s(h[k][0], v1(0));
 #pragma unroll
-                        for (int tt = 1; tt < T; ++tt) {
-                            ar = __fma_rn(h[k][tt], xw[k][tt].x, ar);
-                            ai = __fma_rn(h[k][tt], xw[k][tt].y, ai);
+                            for (int tt = 1; tt < T; ++tt) {
+                                acc0 = fma2s(h[k][tt], v0(tt), acc0);
+                                acc1 = fma2s(h[k][tt], v1(tt), acc1);
+                            }
+                            y0[k] = acc0;
+                            y1[k] = acc1;
                         }
-                        y[k] = make_float2(__double2float_rn(ar), __double2float_rn(ai));
-                    } else {
-                        float2 acc = mul2s(h[k][0], xw[k][0]);
 #pragma unroll
-                        for (int tt = 1; tt < T; ++tt)
-                            acc = fma2s(h[k][tt], xw[k][tt], acc);
-                        y[k] = acc;
+                        for (int tt = 1; tt + 2 < T; ++tt)
+                            xw[k][tt] = xw[k][tt + 2];
+                        if (T >= 3)
+                            xw[k][T - 2] = a;
+                        xw[k][T - 1] = bb;
+                    }
+                    if constexpr (Cfg::TRIV) {
+                        fft_prestages_trivial(y0);
+                        fft_prestages_trivial(y1);
+                    } else {
+                        fft_prestages<L, RLOG>(y0, twr);
+                        fft_prestages<L, RLOG>(y1, twr);
+                    }
+#pragma unroll
+                    for (int k = 0; k < R; ++k) {
+                        tile[i * Cfg::STRIDE + sw(static_cast<unsigned>(k * NTG))] = y0[k];
+                        tile[(i + 1) * Cfg::STRIDE + sw(static_cast<unsigned>(k * NTG))] = y1[k];
+                    }
+                    if constexpr (Cfg::HS) { // this group's rows of the pass group are written
+                        const int r = g * B + i + 1;
+                        if (i + 1 == B - 1 || (r + 1) % Cfg::PROWS == 0)
+                            named_arrive(Cfg::bar_full(t, r / Cfg::PROWS), Cfg::hcount(r / Cfg::PROWS));
                     }
                 }
-                if constexpr (Cfg::TRIV)
-                    fft_prestages_trivial(y);
-                else
-                    fft_prestages<L, RLOG>(y, twr);
-#pragma unroll
-                for (int k = 0; k < R; ++k)
-                    tile[i * Cfg::STRIDE + sw(static_cast<unsigned>(k * NTG))] = y[k];
-                if constexpr (Cfg::HS) { // this group's rows of the pass group are written
-                    const int r = g * B + i;
-                    if (i == B - 1 || (r + 1) % Cfg::PROWS == 0)
-                        named_arrive(Cfg::bar_full(t, r / Cfg::PROWS), Cfg::hcount(r / Cfg::PROWS));
+            } else {
+    #pragma unroll
+                for (int i = 0; i < B; ++i) {
+                    if constexpr (Cfg::HS) { // tile row g*B+i's pass group has drained tile t
+                        const int r = g * B + i;
+                        if ((i == 0 || r % Cfg::PROWS == 0) && b >= Cfg::NTILE)
+                            named_sync(Cfg::bar_empty(t, r / Cfg::PROWS), Cfg::hcount(r / Cfg::PROWS));
+                    }
+                    float2 y[R];
+    #pragma unroll
+                    for (int k = 0; k < R; ++k) {
+                        const float2 x = chunk[i * N + k * NTG];
+    #pragma unroll
+                        for (int tt = 0; tt + 1 < T; ++tt)
+                            xw[k][tt] = xw[k][tt + 1];
+                        xw[k][T - 1].x = static_cast<Acc>(x.x);
+                        xw[k][T - 1].y = static_cast<Acc>(x.y);
+                        if constexpr (Cfg::EXACT) {
+                            double ar = __dmul_rn(h[k][0], xw[k][0].x);
+                            double ai = __dmul_rn(h[k][0], xw[k][0].y);
+    #pragma unroll
+                            for (int tt = 1; tt < T; ++tt) {
+                                ar = __fma_rn(h[k][tt], xw[k][tt].x, ar);
+                                ai = __fma_rn(h[k][tt], xw[k][tt].y, ai);
+                            }
+                            y[k] = make_float2(__double2float_rn(ar), __double2float_rn(ai));
+                        } else {
+                            float2 acc = mul2s(h[k][0], xw[k][0]);
+    #pragma unroll
+                            for (int tt = 1; tt < T; ++tt)
+                                acc = fma2s(h[k][tt], xw[k][tt], acc);
+                            y[k] = acc;
+                        }
+                    }
+                    if constexpr (Cfg::TRIV)
+                        fft_prestages_trivial(y);
+                    else
+                        fft_prestages<L, RLOG>(y, twr);
+    #pragma unroll
+                    for (int k = 0; k < R; ++k)
+                        tile[i * Cfg::STRIDE + sw(static_cast<unsigned>(k * NTG))] = y[k];
+                    if constexpr (Cfg::HS) { // this group's rows of the pass group are written
+                        const int r = g * B + i;
+                        if (i == B - 1 || (r + 1) % Cfg::PROWS == 0)
+                            named_arrive(Cfg::bar_full(t, r / Cfg::PROWS), Cfg::hcount(r / Cfg::PROWS));
+                    }
                 }
             }
             __syncwarp();

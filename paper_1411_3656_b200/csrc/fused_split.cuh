@@ -79,8 +79,15 @@ PPFG_DEV void set_max_regs() {
 }
 
 template <int L_, int LQ_, int T_, bool EXACT_, int FIR_WG_ = 2, int W_ = 5,
-          int FIR_REGS_ = 152, int FFT_REGS_ = 104, int PC_ = 0, bool TW4_ = false, bool HS_ = false>
+          int FIR_REGS_ = 152, int FFT_REGS_ = 104, int PC_ = 0, bool TW4_ = false, bool HS_ = false,
+          bool PAIR_ = false>
 struct SplitCfg {
+    // PAIR: the FIR role filters two consecutive spectra per step with their
+    // accumulation chains interleaved (each output still sums its taps in
+    // ascending order, so results are unchanged): with R <= 2 channels per
+    // thread a single chain per output leaves the FMA pipe waiting on its
+    // own latency
+    static constexpr bool PAIR = PAIR_;
     // HS: the owner tile is handed over per FFT warpgroup (pass group pg owns
     // rows [pg*B/2, (pg+1)*B/2)): local FULL named barrier, remote full
     // mbarrier and the empty mbarriers all per (tile, pass group), so a pass
@@ -140,6 +147,8 @@ struct SplitCfg {
     static constexpr bool POWER_OK = PNT % UL == 0;
     static constexpr int POWER_ROWS = PG * (PNT / UL);
     static_assert(!HS || B % 2 == 0, "HS splits the tile's rows over the two FFT warpgroups");
+    static_assert(!PAIR || (B % 2 == 0 && RB % 2 == 0 && PROWS % 2 == 0 && T >= 2),
+                  "spectrum pairs within a chunk and a pass group");
     static_assert(Q >= 2 && Q <= 8, "portable cluster sizes");
     static_assert(R >= 1 && R <= 8 && R * Q * NFIR == N, "every FIR thread owns whole channels");
     static constexpr int LAUNCH_REGS = (65536 / NT) & ~7;
@@ -382,51 +391,124 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
             }
             const uint32_t ltile_u32 = tile_u32;
             if (tid == 0) PPFG_TR(0, b, 2);
+            if constexpr (Cfg::PAIR) {
 #pragma unroll
-            for (int i = 0; i < B; ++i) {
-                if constexpr (Cfg::HS) { // the owner's pass group i / PROWS has read tile t
-                    if (i % PROWS == 0 && f >= 2)
-                        mbar_wait(empty + (d * 2 + t) * PG + i / PROWS,
-                                  static_cast<uint32_t>(((f >> 1) - 1) & 1));
-                }
-                const uint32_t rbar = rbar0 + 8u * static_cast<uint32_t>(i / PROWS);
-                const float2* chunk = ring + slot[i / Cfg::RB] * Cfg::CHUNK_FLOATS2 +
-                                      (i % Cfg::RB) * (R * RUN) + j;
-                float2 y[R];
+                for (int i = 0; i < B; i += 2) {
+                    if constexpr (Cfg::HS) { // the owner's pass group i / PROWS has read tile t
+                        if (i % PROWS == 0 && f >= 2)
+                            mbar_wait(empty + (d * 2 + t) * PG + i / PROWS,
+                                      static_cast<uint32_t>(((f >> 1) - 1) & 1));
+                    }
+                    const uint32_t rbar = rbar0 + 8u * static_cast<uint32_t>(i / PROWS);
+                    const float2* c0p = ring + slot[i / Cfg::RB] * Cfg::CHUNK_FLOATS2 +
+                                        (i % Cfg::RB) * (R * RUN) + j;
+                    const float2* c1p = ring + slot[(i + 1) / Cfg::RB] * Cfg::CHUNK_FLOATS2 +
+                                        ((i + 1) % Cfg::RB) * (R * RUN) + j;
+                    float2 y0[R], y1[R];
 #pragma unroll
-                for (int k = 0; k < R; ++k) {
-                    const float2 x = chunk[k * RUN];
+                    for (int k = 0; k < R; ++k) {
+                        // window convention: xw[k][t] = x[i + t - 1], t = 1..T-1; output i
+                        // reads (xw[1..T-1], a), output i+1 (xw[2..T-1], a, b)
+                        const float2 xa = c0p[k * RUN], xb = c1p[k * RUN];
+                        Win a, bb;
+                        a.x = static_cast<Acc>(xa.x);
+                        a.y = static_cast<Acc>(xa.y);
+                        bb.x = static_cast<Acc>(xb.x);
+                        bb.y = static_cast<Acc>(xb.y);
+                        auto v0 = [&](int tt) -> Win { return tt + 1 <= T - 1 ? xw[k][tt + 1] : a; };
+                        auto v1 = [&](int tt) -> Win {
+                            return tt + 2 <= T - 1 ? xw[k][tt + 2] : (tt + 2 == T ? a : bb);
+                        };
+                        if constexpr (Cfg::EXACT) {
+                            double ar0 = __dmul_rn(h[k][0], v0(0).x), ai0 = __dmul_rn(h[k][0], v0(0).y);
+                            double ar1 = __dmul_rn(h[k][0], v1(0).x), ai1 = __dmul_rn(h[k][0], v1(0).y);
 #pragma unroll
-                    for (int tt = 0; tt + 1 < T; ++tt)
-                        xw[k][tt] = xw[k][tt + 1];
-                    xw[k][T - 1].x = static_cast<Acc>(x.x);
-                    xw[k][T - 1].y = static_cast<Acc>(x.y);
-                    if constexpr (Cfg::EXACT) {
-                        double ar = __dmul_rn(h[k][0], xw[k][0].x);
-                        double ai = __dmul_rn(h[k][0], xw[k][0].y);
+                            for (int tt = 1; tt < T; ++tt) {
+                                ar0 = __fma_rn(h[k][tt], v0(tt).x, ar0);
+                                ai0 = __fma_rn(h[k][tt], v0(tt).y, ai0);
+                                ar1 = __fma_rn(h[k][tt], v1(tt).x, ar1);
+                                ai1 = __fma_rn(h[k][tt], v1(tt).y, ai1);
+                            }
+                            y0[k] = make_float2(__double2float_rn(ar0), __double2float_rn(ai0));
+                            y1[k] = make_float2(__double2float_rn(ar1), __double2float_rn(ai1));
+                        } else {
+                            float2 acc0 = mul2s(h[k][0], v0(0)), acc1 = mul2s(h[k][0], v1(0));
 #pragma unroll
-                        for (int tt = 1; tt < T; ++tt) {
-                            ar = __fma_rn(h[k][tt], xw[k][tt].x, ar);
-                            ai = __fma_rn(h[k][tt], xw[k][tt].y, ai);
+                            for (int tt = 1; tt < T; ++tt) {
+                                acc0 = fma2s(h[k][tt], v0(tt), acc0);
+                                acc1 = fma2s(h[k][tt], v1(tt), acc1);
+                            }
+                            y0[k] = acc0;
+                            y1[k] = acc1;
                         }
-                        y[k] = make_float2(__double2float_rn(ar), __double2float_rn(ai));
-                    } else {
-                        float2 acc = mul2s(h[k][0], xw[k][0]);
 #pragma unroll
-                        for (int tt = 1; tt < T; ++tt)
-                            acc = fma2s(h[k][tt], xw[k][tt], acc);
-                        y[k] = acc;
+                        for (int tt = 1; tt + 2 < T; ++tt)
+                            xw[k][tt] = xw[k][tt + 2];
+                        if (T >= 3)
+                            xw[k][T - 2] = a;
+                        xw[k][T - 1] = bb;
+                    }
+                    fft_prestages<Cfg::L, RLOG>(y0, twr);
+                    fft_prestages<Cfg::L, RLOG>(y1, twr);
+#pragma unroll
+                    for (int k = 0; k < R; ++k) {
+                        const uint32_t off0 = 8u * (i * Cfg::STRIDE + slot_of[k]);
+                        const uint32_t off1 = off0 + 8u * Cfg::STRIDE;
+                        st_local_or_async_f2(local, ltile_u32 + off0, rtile + off0, y0[k], rbar);
+                        st_local_or_async_f2(local, ltile_u32 + off1, rtile + off1, y1[k], rbar);
+                    }
+                    if constexpr (Cfg::HS) { // own block of pass group i / PROWS written
+                        if (local && (i + 2) % PROWS == 0)
+                            named_arrive(1 + t * PG + i / PROWS, NFIR + PNT);
                     }
                 }
-                fft_prestages<Cfg::L, RLOG>(y, twr);
-#pragma unroll
-                for (int k = 0; k < R; ++k) {
-                    const uint32_t off = 8u * (i * Cfg::STRIDE + slot_of[k]);
-                    st_local_or_async_f2(local, ltile_u32 + off, rtile + off, y[k], rbar);
-                }
-                if constexpr (Cfg::HS) { // own block of pass group i / PROWS written
-                    if (local && (i + 1) % PROWS == 0)
-                        named_arrive(1 + t * PG + i / PROWS, NFIR + PNT);
+            } else {
+    #pragma unroll
+                for (int i = 0; i < B; ++i) {
+                    if constexpr (Cfg::HS) { // the owner's pass group i / PROWS has read tile t
+                        if (i % PROWS == 0 && f >= 2)
+                            mbar_wait(empty + (d * 2 + t) * PG + i / PROWS,
+                                      static_cast<uint32_t>(((f >> 1) - 1) & 1));
+                    }
+                    const uint32_t rbar = rbar0 + 8u * static_cast<uint32_t>(i / PROWS);
+                    const float2* chunk = ring + slot[i / Cfg::RB] * Cfg::CHUNK_FLOATS2 +
+                                          (i % Cfg::RB) * (R * RUN) + j;
+                    float2 y[R];
+    #pragma unroll
+                    for (int k = 0; k < R; ++k) {
+                        const float2 x = chunk[k * RUN];
+    #pragma unroll
+                        for (int tt = 0; tt + 1 < T; ++tt)
+                            xw[k][tt] = xw[k][tt + 1];
+                        xw[k][T - 1].x = static_cast<Acc>(x.x);
+                        xw[k][T - 1].y = static_cast<Acc>(x.y);
+                        if constexpr (Cfg::EXACT) {
+                            double ar = __dmul_rn(h[k][0], xw[k][0].x);
+                            double ai = __dmul_rn(h[k][0], xw[k][0].y);
+    #pragma unroll
+                            for (int tt = 1; tt < T; ++tt) {
+                                ar = __fma_rn(h[k][tt], xw[k][tt].x, ar);
+                                ai = __fma_rn(h[k][tt], xw[k][tt].y, ai);
+                            }
+                            y[k] = make_float2(__double2float_rn(ar), __double2float_rn(ai));
+                        } else {
+                            float2 acc = mul2s(h[k][0], xw[k][0]);
+    #pragma unroll
+                            for (int tt = 1; tt < T; ++tt)
+                                acc = fma2s(h[k][tt], xw[k][tt], acc);
+                            y[k] = acc;
+                        }
+                    }
+                    fft_prestages<Cfg::L, RLOG>(y, twr);
+    #pragma unroll
+                    for (int k = 0; k < R; ++k) {
+                        const uint32_t off = 8u * (i * Cfg::STRIDE + slot_of[k]);
+                        st_local_or_async_f2(local, ltile_u32 + off, rtile + off, y[k], rbar);
+                    }
+                    if constexpr (Cfg::HS) { // own block of pass group i / PROWS written
+                        if (local && (i + 1) % PROWS == 0)
+                            named_arrive(1 + t * PG + i / PROWS, NFIR + PNT);
+                    }
                 }
             }
             if (tid == 0) PPFG_TR(0, b, 3);

@@ -11,6 +11,9 @@ std::vector<FusedEntry> fused_part_split() {
     // 0.416 -> 0.420; not EXACT C=2048 (0.474 -> 0.463). Register splits with
     // HS (two A/B rounds): C=4096 FIR/FFT 168/88 0.537 -> 0.562; 128/128 and
     // 144/112 elsewhere, and flipping the float4 twiddles, all measured slower.
+    // Paired FIR chains (SplitCfg PAIR, 12th argument) where they helped: EXACT
+    // T=16 0.41 -> 0.428, EXACT C=2048 0.474 -> 0.481 (FAST T=16, C=2048 and
+    // EXACT T=8 lost 1-4 %).
     return {
         // thread-block clusters, FIR split by channel block and FFT by
         // spectrum (fused_split.cuh) — for FIR state that does not fit one SM.
@@ -34,9 +37,9 @@ std::vector<FusedEntry> fused_part_split() {
         split_entry<SplitCfg<10, 1, 16, false, 2, 5, 136, 120, 0, true, true>>(true),
         split_entry<SplitCfg<10, 2, 32, false, 2, 5, 152, 104, 0, true, true>>(false),
         split_entry<SplitCfg<10, 1, 8, true, 2, 5, 136, 120, 0, true, true>>(true),
-        split_entry<SplitCfg<10, 2, 16, true, 2, 5, 152, 104, 0, true, true>>(true),
+        split_entry<SplitCfg<10, 2, 16, true, 2, 5, 152, 104, 0, true, true, true>>(true),
         split_entry<SplitCfg<11, 1, 8, false, 2, 5, 136, 120, 0, false, true>>(true),
-        split_entry<SplitCfg<11, 2, 8, true, 2, 5, 152, 104, 0, true>>(true),
+        split_entry<SplitCfg<11, 2, 8, true, 2, 5, 152, 104, 0, true, false, true>>(true),
         split_entry<SplitCfg<12, 2, 8, false, 2, 5, 168, 88, 0, false, true>>(true),
         split_entry<SplitCfg<13, 3, 8, false>>(false),
     };
