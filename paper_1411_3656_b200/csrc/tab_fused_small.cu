@@ -9,9 +9,9 @@ std::vector<FusedEntry> fused_part_small() {
         fused_entry<FusedCfg<8, 16, 1, false, 160, 96, 4, 2, 2, false, 0, true>>(),
         fused_entry<FusedCfg<7, 16, 0, false, 160, 96, 4, 2, 2, false, 0, true>>(),
         fused_entry<FusedCfg<6, 16, 1, false, 160, 96, 4, 2, 2, false, 0, true>>(),
-        fused_entry<FusedCfg<8, 16, 0, true, 160, 96, 4, 2, 2, false, 0, true>>(),
-        fused_entry<FusedCfg<7, 16, 0, true, 160, 96, 4, 2, 2, false, 0, true>>(),
-        fused_entry<FusedCfg<6, 16, 0, true, 160, 96, 4, 2, 2, false, 0, true>>(),
+        fused_entry<FusedCfg<8, 16, 0, true, 160, 96, 4, 2, 2, false, 0, true, false, true>>(),
+        fused_entry<FusedCfg<7, 16, 0, true, 160, 96, 4, 2, 2, false, 0, true, false, true>>(),
+        fused_entry<FusedCfg<6, 16, 0, true, 160, 96, 4, 2, 2, false, 0, true, false, true>>(),
         fused_entry<FusedCfg<9, 4, 2, false>>(),
         fused_entry<FusedCfg<8, 4, 0, false, 160, 96, 4, 2, 2, false, 0, true>>(),
         fused_entry<FusedCfg<7, 4, 2, false>>(),
