@@ -169,3 +169,15 @@ def test_multi_device_empty_segment_with_null_buffers(cuda, port):
     assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
     for p in plans:
         p.close()
+
+
+def test_dropin_stream_exceptions_reach_the_caller(cuda):
+    """C++ drop-in process_stream with throwing istream / ostream: the
+    exception (or decode_error at the byte offset) reaches the caller, after
+    the bytes delivered before the failure were processed (tests/cpp)."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.abspath(__file__)), "cpp", "stream_exceptions")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.count("ok:") == 3, r.stdout
