@@ -113,6 +113,14 @@ struct SplitCfg {
     static constexpr int BU = ilcm(B, T) / B; // batches per unrolled FIR body (window renaming)
     static constexpr int BQ = ilcm(BU, Q);    // n_batches granule: whole bodies, equal fills per CTA
     static constexpr int RUN = NFIR;          // channels per contiguous input run
+    // the TMA view of the input: R runs of RUN channels (box {RUN, R, RB} at
+    // {rank*RUN, 0, row}); a run longer than the 256-element box limit (R = 1
+    // with 4 FIR warpgroups) is fetched as TSPLIT sub-runs of 256 instead
+    // (view of N/256 runs, box {256, TSPLIT, RB} at {0, rank*TSPLIT, row})
+    static constexpr int TSPLIT = RUN > 256 ? RUN / 256 : 1;
+    static constexpr int MAP_RUN = TSPLIT > 1 ? 256 : RUN;
+    static constexpr int MAP_R = TSPLIT > 1 ? N / 256 : R;      // runs in the view
+    static constexpr int MAP_BOX_R = TSPLIT > 1 ? TSPLIT : R;   // runs per copy
     static constexpr unsigned STRIDE = sw_row_stride(N);
     static constexpr size_t TILE_FLOATS2 = size_t(B) * STRIDE;
     static constexpr size_t TILE_BYTES = sizeof(float2) * TILE_FLOATS2;
@@ -156,7 +164,8 @@ struct SplitCfg {
     static_assert(SMEM <= 232448, "shared memory per CTA");
     static_assert(PC >= 2, "input ring too shallow");
     static_assert(B % RB == 0, "whole chunks per batch");
-    static_assert(RUN <= 256 && R <= 256 && RB <= 256, "TMA box dimensions");
+    static_assert(MAP_RUN <= 256 && MAP_BOX_R <= 256 && RB <= 256, "TMA box dimensions");
+    static_assert(TSPLIT == 1 || (R == 1 && RUN % 256 == 0), "sub-run TMA view: one channel per thread");
     static_assert(BU * B <= 64, "FIR unroll too large");
 };
 
@@ -299,7 +308,9 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
     const long long n_chunks = (rows + Cfg::RB - 1) / Cfg::RB;
     auto issue = [&](long long c, int slot) {
         mbar_arrive_expect_tx(ring_full + slot, static_cast<uint32_t>(Cfg::CHUNK_BYTES));
-        tma_load_3d(ring + slot * Cfg::CHUNK_FLOATS2, &in_map, static_cast<int>(rank * RUN), 0,
+        tma_load_3d(ring + slot * Cfg::CHUNK_FLOATS2, &in_map,
+                    Cfg::TSPLIT > 1 ? 0 : static_cast<int>(rank * RUN),
+                    Cfg::TSPLIT > 1 ? static_cast<int>(rank * Cfg::TSPLIT) : 0,
                     static_cast<int>(o0 + T - 1 + c * Cfg::RB), ring_full + slot);
     };
     if (producer) {

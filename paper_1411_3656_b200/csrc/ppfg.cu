@@ -454,13 +454,13 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 // moved untouched), dims {C/R channels, R runs, S_in spectra}; a box
 // {RUN, R, RB} at {rank*RUN, 0, row} is RB spectra x R runs of RUN channels.
 int encode_input_map(CUtensorMap* map, const float2* din, uint64_t C, uint64_t S_in, int r, int rb,
-                     int run) {
+                     int run, int box_r) {
     PFN_cuTensorMapEncodeTiled_v12000 encode = tensor_map_encoder();
     if (!encode)
         return fail(PPFG_CUDA_ERROR, "cuTensorMapEncodeTiled is not available from the driver");
     const cuuint64_t dims[3] = {C / r, static_cast<cuuint64_t>(r), S_in};
     const cuuint64_t strides[2] = {C / r * sizeof(float2), C * sizeof(float2)};
-    const cuuint32_t box[3] = {static_cast<cuuint32_t>(run), static_cast<cuuint32_t>(r),
+    const cuuint32_t box[3] = {static_cast<cuuint32_t>(run), static_cast<cuuint32_t>(box_r),
                                static_cast<cuuint32_t>(rb)};
     const cuuint32_t estr[3] = {1, 1, 1};
     const CUresult res = encode(map, CU_TENSOR_MAP_DATA_TYPE_INT64, 3, const_cast<float2*>(din), dims,
@@ -527,7 +527,7 @@ int launch_fused_entry(ppfg_plan p, const FusedEntry* e, const float* taps, uint
         long long rows_per_cluster = static_cast<long long>(cdiv(S_out, n_clusters));
         if (e->map_r > 0) {
             CUtensorMap map;
-            PPFG_TRY(encode_input_map(&map, din, p->C, S_in, e->map_r, e->map_rb, e->map_run));
+            PPFG_TRY(encode_input_map(&map, din, p->C, S_in, e->map_r, e->map_rb, e->map_run, e->map_box_r));
             void* tw = e->tw4 ? static_cast<void*>(p->d_tw4) : static_cast<void*>(p->d_tw);
             void* args[] = {&map, &din, &dout, &S_out_ll, &rows_per_cluster, &taps, &tw};
             PPFG_CUDA(cudaLaunchKernelExC(&cfg, fn, args));

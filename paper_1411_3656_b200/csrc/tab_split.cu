@@ -13,7 +13,9 @@ std::vector<FusedEntry> fused_part_split() {
     // 144/112 elsewhere, and flipping the float4 twiddles, all measured slower.
     // Paired FIR chains (SplitCfg PAIR, 12th argument) where they helped: EXACT
     // T=16 0.41 -> 0.428, EXACT C=2048 0.474 -> 0.481 (FAST T=16, C=2048 and
-    // EXACT T=8 lost 1-4 %).
+    // EXACT T=8 lost 1-4 %). Four FIR warpgroups with one channel per thread
+    // (the TSPLIT input view): EXACT T=8 0.645 -> 0.53-0.54, FAST T=16 (W=4)
+    // 0.70 -> 0.70 / (W=5) 0.55 — the smaller FFT role (80 registers) loses.
     return {
         // thread-block clusters, FIR split by channel block and FFT by
         // spectrum (fused_split.cuh) — for FIR state that does not fit one SM.

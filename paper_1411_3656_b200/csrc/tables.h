@@ -20,8 +20,9 @@ struct FusedEntry {
     int q;              // CTAs per cluster (1: single-SM kernel)
     bool preferred;     // cluster kernels: faster than FIR -> HBM -> FFT (measured)
     int map_r = 0;      // > 0: the kernel reads its input through a 3-D TMA tensor
-    int map_rb = 0;     //      map with box {map_run, map_r, map_rb} (fused_split.cuh)
-    int map_run = 0;
+    int map_rb = 0;     //      map of map_r runs of C/map_r channels, box {map_run,
+    int map_run = 0;    //      map_box_r, map_rb} (fused_split.cuh)
+    int map_box_r = 0;
     KernelFn power_fn = nullptr; // detection variant (POWER), single-SM entries
     int power_rows = 0;          // its partials per CTA (tile rows)
     bool tw4 = false;            // takes the pre-expanded float4 twiddle table

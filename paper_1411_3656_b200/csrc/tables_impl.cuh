@@ -48,7 +48,7 @@ template <class Cfg>
 FusedEntry split_entry(bool preferred) {
     FusedEntry e{Cfg::L,    Cfg::T,  Cfg::EXACT, reinterpret_cast<KernelFn>(&fused_split_kernel<Cfg>),
                  Cfg::SMEM, Cfg::NT, Cfg::B,     Cfg::Q,
-                 preferred, Cfg::R,  Cfg::RB,    Cfg::RUN};
+                 preferred, Cfg::MAP_R, Cfg::RB, Cfg::MAP_RUN, Cfg::MAP_BOX_R};
     e.tw4 = Cfg::TW4;
     e.sig = __PRETTY_FUNCTION__;
     if constexpr (Cfg::POWER_OK) {
