@@ -297,6 +297,7 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
     using tap_t = typename std::conditional<Cfg::EXACT, double, float>::type;
     long long waited = 0; // input chunks whose arrival this thread has waited for
     int cb_prev = -1;
+    int pending = -1;     // ring slot of the item whose publication is deferred
     tap_t h[T];
     for (long long m = 0; m < my_items; ++m) {
         const long long item = blockIdx.x + m * grid;
@@ -383,6 +384,12 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
                     }
                 }
             }
+            if (st == 0 && pending >= 0) { // the previous item's publication (above)
+                __syncwarp();
+                if (lane == 0)
+                    red_release_gpu_add(produced + pending, 1);
+                pending = -1;
+            }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 float2 y;
@@ -398,19 +405,24 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
 #endif
             }
         }
-        // publish the item per warp: the warp's ring stores, then one
-        // GPU-scope release add by its lane 0 (the FFT role waits for
-        // NWF * C/32 of them per chunk) — a release waits for the releasing
-        // warp's own stores only, so the warps do not serialise on one fence
+        // publish the item per warp: one GPU-scope release add by its lane 0
+        // (the FFT role waits for NWF * C/32 of them per chunk). It is
+        // deferred to the next item's first step (after its FMAs, before its
+        // stores): a release waits for the releasing warp's earlier stores,
+        // which by then have drained, so the publication costs no stall
         __syncwarp();
         if (tid == 0)
             L2X_TR(0, 5, static_cast<int>(m));
-        if (lane == 0)
-            red_release_gpu_add(produced + slot, 1);
+        pending = slot;
         named_sync(BAR_FIR, NFIR); // every warp is done with the item's input chunks
         if (tid == 0) // refill the released slots
             for (; issued < my_chunks && issued < g0 + NIC + NS; ++issued)
                 issue(issued);
+    }
+    if (pending >= 0) { // the last item
+        __syncwarp();
+        if (lane == 0)
+            red_release_gpu_add(produced + pending, 1);
     }
 }
 

@@ -736,6 +736,10 @@ bool launch_tiny(ppfg_plan p, const float2* din, uint64_t S_in, float2* dout, cu
 // the plan (counters zeroed per launch; launches sharing them are ordered)
 int launch_l2x(ppfg_plan p, const float2* din, uint64_t S_in, float2* dout, cudaStream_t st) {
     const L2xEntry* e = p->l2x;
+    // a CTA's consecutive work items lie grid / (C/32) chunks apart; the
+    // deferred publication (l2x.cuh) needs that well inside the ring
+    if (static_cast<uint64_t>(p->num_sms) / (p->C / 32) + 2 > static_cast<uint64_t>(e->nsr))
+        return fail(PPFG_CONFIG_ERROR, "fused fir+fft (L2 exchange): ring too small for this grid");
     // counters [2 * nsr], the trace flag, then (at +256 B) the debug timeline
     const char* trace_path = std::getenv("PPFG_L2X_TRACE");
     constexpr size_t kTraceBytes = sizeof(unsigned long long) * 2 * 8 * 256;
