@@ -35,6 +35,17 @@ def timeit(fn, reps=5, warm=2):
     torch.cuda.synchronize()
     ts = []
     s = torch.cuda.current_stream()
+    if os.environ.get("PPFG_B2B"):   # back to back: the host's submission gap hidden
+        ev = []
+        for _ in range(reps + 1):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            fn()
+            b.record(s)
+            ev.append((a, b))
+        torch.cuda.synchronize()
+        return float(np.median([a.elapsed_time(b) for a, b in ev[1:]])) / 1e3
     for _ in range(reps):
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)

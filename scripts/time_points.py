@@ -27,9 +27,13 @@ for spec in sys.argv[1:]:
         with ppf.Plan(C, T, c) as p:
             t = timeit(lambda: p.fir(x, out=y))
         B = (2 * S - T + 1) * C * 8
-    elif mode == "fft":
+    elif mode in ("fft", "fft-oop"):   # channelize_block, in place / out of place
+        z = x if mode == "fft" else torch.empty_like(x)
         with ppf.Plan(C, 1, ppf.generate_prototype(C, 1)) as p:
-            t = timeit(lambda: p.channelize(x, out=x))
+            t = timeit(lambda: p.channelize(x, out=z))
+        B = 2 * S * C * 8
+    elif mode == "cufft":
+        t = timeit(lambda: torch.fft.fft(x, dim=1))
         B = 2 * S * C * 8
     else:
         with ppf.Plan(C, T, c, flags=FL[mode]) as p:
