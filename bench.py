@@ -365,23 +365,29 @@ def time_steps(step, stream, steps):
 
 
 def _median_time(fn, reps=5, warm=2):
-    """Median device time of fn() over reps (CUDA events on torch's current
-    stream, which the library's calls run on), after warm-ups."""
+    """Median device time of one fn() launch, CUDA events on torch's current
+    stream (which the library's calls run on), after warm-ups. The reps are
+    queued back to back and synchronised once: each launch's events then
+    bracket the kernel alone, not the host's submission of the next call (a
+    synchronise after every rep would add the ~10 us host path of a library
+    call to each 0.3 ms point); the first rep, queued behind an idle GPU, is
+    dropped. Inputs are >= 512 MiB (> the 126 MB L2), so no rep finds the
+    previous one's data in cache."""
     import torch
     for _ in range(warm):
         fn()
     torch.cuda.synchronize()
     s = torch.cuda.current_stream()
-    ts = []
-    for _ in range(reps):
+    ev = []
+    for _ in range(reps + 1):
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(s)
         fn()
         b.record(s)
-        torch.cuda.synchronize()
-        ts.append(a.elapsed_time(b) / 1e3)
-    return float(np.median(ts))
+        ev.append((a, b))
+    torch.cuda.synchronize()
+    return float(np.median([a.elapsed_time(b) for a, b in ev[1:]])) / 1e3
 
 
 def config_points(dev, peak, long_bytes):
@@ -668,7 +674,7 @@ def main():
         t0 = time.perf_counter()
         configs = {"points": config_points(dev, peak, int(args.long_gb * 1e9)),
                    "peak_gbps": peak, "seconds": None,
-                   "timing": "median of 5 after 2 warm-ups, CUDA events, device-resident; "
+                   "timing": "median of 5 back-to-back launches after 2 warm-ups, CUDA events, device-resident; "
                              "1 GiB points, cfg1 and long16 at their full size"}
         configs["seconds"] = time.perf_counter() - t0
 
