@@ -28,10 +28,21 @@ def _nvcc():
     return "nvcc"
 
 
+# host-only C++ units (compiled by nvcc as plain C++, per-unit ISA flags)
+HOST_FLAGS = {"hostcopy.cpp": ["-Xcompiler", "-mavx2"]}
+
+
 def units():
-    """The translation units: ppfg.cu (host code + small kernels) and the
-    tab_*.cu kernel-table units, compiled in parallel."""
-    return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+    """The translation units: ppfg.cu (host code + small kernels), the
+    tab_*.cu kernel-table units and the host-only *.cpp units, compiled in
+    parallel."""
+    return sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
+
+
+def compile_cmd(src, obj):
+    """nvcc command compiling one unit (a .cpp unit is host C++ only)."""
+    extra = HOST_FLAGS.get(os.path.basename(src), [])
+    return [_nvcc(), *NVCC_FLAGS, *extra, "-I" + INCLUDE, "-c", "-o", obj, src]
 
 
 def headers():
@@ -51,7 +62,7 @@ def stale() -> bool:
 
 
 def _obj(cu):
-    return os.path.join(OBJ_DIR, os.path.basename(cu)[:-3] + ".o")
+    return os.path.join(OBJ_DIR, os.path.splitext(os.path.basename(cu))[0] + ".o")
 
 
 def build(force: bool = False, verbose: bool = False, jobs: int = 0) -> str:
@@ -67,7 +78,7 @@ def build(force: bool = False, verbose: bool = False, jobs: int = 0) -> str:
                 os.path.getmtime(cu), newest_header):
             return obj
         tmp = obj + f".tmp{os.getpid()}"
-        cmd = [_nvcc(), *NVCC_FLAGS, "-I" + INCLUDE, "-c", "-o", tmp, cu]
+        cmd = compile_cmd(cu, tmp)
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.check_call(cmd)

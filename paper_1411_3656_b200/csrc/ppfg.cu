@@ -29,6 +29,10 @@
 #include "fused.cuh"
 #include "fused_split.cuh"
 
+namespace ppfg {
+void copy_piece(void* dst, const void* src, size_t n); // hostcopy.cpp
+}
+
 namespace {
 
 using namespace ppfg;
@@ -907,10 +911,12 @@ int run_mean_power(ppfg_plan p, bool fused, const void* in, uint64_t n_rows, dou
 
 // ------------------------------------------------------ host copy pool
 // Pageable callers (the reference API hands over std::vectors) pay a host
-// copy into / out of pinned staging per call; one core copies ~10-15 GB/s,
+// copy into / out of pinned staging per call; one core copies ~8-10 GB/s,
 // below PCIe, so large copies are split over a small process-wide pool of
 // worker threads (they also take the first-touch page faults of freshly
-// allocated output vectors in parallel).
+// allocated output vectors in parallel). Each piece is copied by
+// ppfg::copy_piece (hostcopy.cpp: streaming stores for large pieces).
+
 class CopyPool {
 public:
     static CopyPool& get() {
@@ -918,9 +924,10 @@ public:
         return *p;
     }
     void copy(void* dst, const void* src, size_t bytes) {
-        constexpr size_t kPiece = size_t(2) << 20;
+        // 1 MiB pieces: an 8 MiB staging chunk goes to all 8 threads
+        constexpr size_t kPiece = size_t(1) << 20;
         if (bytes < 2 * kPiece || n_workers_ == 0) {
-            std::memcpy(dst, src, bytes);
+            ppfg::copy_piece(dst, src, bytes);
             return;
         }
         std::lock_guard<std::mutex> one(job_mu_); // one parallel copy at a time
@@ -928,7 +935,7 @@ public:
         job_dst_ = static_cast<char*>(dst);
         job_src_ = static_cast<const char*>(src);
         job_bytes_ = bytes;
-        job_per_ = (bytes / parts + 63) & ~size_t(63);
+        job_per_ = ((bytes + parts - 1) / parts + 63) & ~size_t(63); // parts * per >= bytes
         job_parts_ = parts;
         done_.store(0, std::memory_order_relaxed);
         const uint64_t g = ++gen_;
@@ -963,7 +970,7 @@ private:
                 continue;
             const size_t o = (v & 0xffffffffu) * job_per_;
             if (o < job_bytes_)
-                std::memcpy(job_dst_ + o, job_src_ + o, std::min(job_per_, job_bytes_ - o));
+                ppfg::copy_piece(job_dst_ + o, job_src_ + o, std::min(job_per_, job_bytes_ - o));
             ++finished;
         }
         if (finished && done_.fetch_add(finished, std::memory_order_acq_rel) + finished == job_parts_) {

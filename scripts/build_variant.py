@@ -20,6 +20,7 @@ d = tempfile.mkdtemp()
 src = os.path.join(d, "csrc")
 shutil.copytree(B.CSRC, src)
 files = sorted(glob.glob(os.path.join(src, "*.cu")) + glob.glob(os.path.join(src, "*.cuh")) +
+               glob.glob(os.path.join(src, "*.cpp")) +
                glob.glob(os.path.join(src, "*.h")))
 if expr.startswith("git:"):  # git:REV — the csrc sources of that revision
     rev = expr[4:]
@@ -35,9 +36,9 @@ print("changed:", [os.path.basename(f) for f in changed])
 hdr_changed = any(not f.endswith(".cu") for f in changed)
 objs = []
 todo = []
-for cu in sorted(glob.glob(os.path.join(src, "*.cu"))):
+for cu in sorted(glob.glob(os.path.join(src, "*.cu")) + glob.glob(os.path.join(src, "*.cpp"))):
     if hdr_changed or cu in changed:
-        o = os.path.join(d, os.path.basename(cu)[:-3] + ".o")
+        o = os.path.join(d, os.path.splitext(os.path.basename(cu))[0] + ".o")
         todo.append((cu, o))
         objs.append(o)
     else:
@@ -46,7 +47,7 @@ for cu in sorted(glob.glob(os.path.join(src, "*.cu"))):
 
 def cc(job):
     cu, o = job
-    subprocess.check_call([B._nvcc(), *B.NVCC_FLAGS, "-I" + B.INCLUDE, "-c", "-o", o, cu])
+    subprocess.check_call(B.compile_cmd(cu, o))
 
 
 with ThreadPoolExecutor(max_workers=8) as ex:

@@ -125,3 +125,20 @@ def test_new_entry_points_validate_arguments_without_a_gpu():
     st = _lib.StreamState()
     assert lib.ppfg_process_stream(None, 4096, 0, 1, _lib.READ_FN(0), None, _lib.WRITE_FN(0), None,
                                    C.byref(st)) == CONFIG_ERROR
+
+
+@pytest.mark.parametrize("n,off", [(0, 0), (1, 1), (300_001, 3), ((1 << 20) + 3, 1),
+                                   ((5 << 20) + 17, 5), ((33 << 20) + 5, 7)])
+def test_host_copy_pool_copies_every_byte(n, off):
+    """ppfg_host_copy (the pageable staging copy: a thread pool, streaming
+    stores for large pieces, hostcopy.cpp) on unaligned ragged sizes — no GPU
+    involved. The bytes around the destination stay untouched."""
+    from paper_1411_3656_b200 import _lib
+    lib = _lib.load()
+    rng = np.random.default_rng(n)
+    src = rng.integers(0, 256, n + 64, dtype=np.uint8)
+    dst = np.full(n + 64, 0xA5, np.uint8)
+    rc = lib.ppfg_host_copy(dst.ctypes.data + off, src.ctypes.data + (off * 3) % 32, n)
+    assert rc == 0
+    assert np.array_equal(dst[off:off + n], src[(off * 3) % 32:(off * 3) % 32 + n])
+    assert (dst[:off] == 0xA5).all() and (dst[off + n:] == 0xA5).all()
