@@ -560,3 +560,30 @@ def test_misaligned_device_views(cuda, port, C, T, flags):
     assert np.array_equal(bits(fir), bits(port.fir(x, C, T, coeffs)))
     assert np.array_equal(bits(chan), bits(port.channelize(x, C)))
     assert _rel(mp.cpu().numpy(), port.mean_power(port.fir_fft(x, C, T, coeffs), C)) <= 2e-5 * np.log2(C)
+
+
+# EXACT mode converts samples to double and results to float on the integer
+# pipe (common.cuh f2d_alu / d2f_alu) with a hardware fallback for the values
+# that path does not cover: zeros of both signs, float subnormals in and out,
+# magnitudes at the ends of the float range, and all-zero stretches (zero
+# outputs) must come out bit-identical to the reference.
+@pytest.mark.parametrize("C,T", [(1024, 8), (512, 8), (64, 8), (1024, 16), (256, 4), (2048, 8),
+                                 (8, 8), (1024, 32)])
+def test_exact_special_values_bitwise(cuda, port, C, T):
+    ppf = ppf_mod()
+    rng = np.random.default_rng(C + T)
+    S = 300 + T
+    x = uniform(rng, S * C).reshape(S, C).copy()
+    xr = x.view(np.float32).reshape(S, C, 2)
+    xr[5:5 + T + 3] = 0.0                                   # a zero stretch: zero outputs
+    xr[40:60, :, 0] = -0.0                                  # negative zeros
+    xr[70:90] *= np.float32(1e-39)                          # subnormal inputs
+    xr[100:110] = rng.choice([1e-45, -1e-45, 3e-44], size=xr[100:110].shape).astype(np.float32)
+    xr[120:130] *= np.float32(1e34)                         # large magnitudes (no FFT overflow)
+    xr[140:150, :, 1] *= np.float32(1e-30)                  # results with tiny imaginary parts
+    coeffs = port.generate_prototype(C, T, 9.0)
+    want = port.fir_fft(x, C, T, coeffs).view(np.complex64).reshape(-1, C)
+    for flags in (ppf.EXACT, ppf.EXACT | ppf.UNFUSED):
+        with ppf.Plan(C, T, coeffs, flags=flags) as p:
+            got = p.fir_fft(x)
+        assert np.array_equal(bits(got), bits(want)), (C, T, flags, p.kernel_name)
