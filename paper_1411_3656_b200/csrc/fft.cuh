@@ -358,6 +358,94 @@ __global__ void __launch_bounds__(FftRing<L, W, NT_>::NT, 1)
     }
 }
 
+// K2n: channelize_block for 64 <= C <= 4096 as a NON-persistent grid of small
+// CTAs, one tile of NR rows each (NR * C * 8 B = 16-64 KB), several CTAs per
+// SM, dispatched in row order. Each CTA loads its rows with one TMA bulk copy
+// per row into a swizzled-row slot, runs the first pass from the natural-order
+// rows (one unit per thread: NT = NR * U0), writes it back in place at
+// swizzled slots, then the remaining passes (FftPasses) and stores the bins.
+// Twiddles: each CTA copies the table into shared memory while its rows land
+// (read straight from global the compiler hoists a pass's twiddle loads and
+// spills). Same
+// butterflies as K2 / K2r / K3: bit-exact. The grid sweeps HBM as one narrow
+// front, the access pattern that streamed fastest of everything measured here
+// (profiles/round2/probes: a non-persistent block copy 6.78 TB/s vs 6.0-6.4
+// persistent).
+template <int L, int W, int NT, int UPT = 1>
+struct FftTiles {
+    using S = FftSchedule<L, W>;
+    static constexpr int N = 1 << L;
+    static constexpr int W0 = S::width(0), LO0 = S::lo(0);
+    static constexpr int U0 = N >> W0;               // first-pass units per row
+    static constexpr int NR = UPT * NT / U0;         // rows per CTA: UPT units per thread
+    static constexpr unsigned STRIDE = sw_row_stride(N);
+    static constexpr size_t TW_BYTES = (sizeof(float2) * N + 127) & ~size_t(127);
+    static constexpr size_t SMEM = TW_BYTES + sizeof(float2) * size_t(NR) * STRIDE;
+    static_assert((UPT * NT) % U0 == 0 && NR >= 1, "whole rows of first-pass units");
+    static_assert(S::NP >= 2, "pass 1 hands over to FftPasses<.., I = 1>");
+};
+
+template <int L, int W, int NT, int MINB = 1, int UPT = 1>
+__global__ void __launch_bounds__(NT, MINB) fft_tiles_kernel(const float2* __restrict__ in,
+                                                       float2* __restrict__ out, long long n_rows,
+                                                       const float2* __restrict__ tw_g) {
+    using F = FftTiles<L, W, NT, UPT>;
+    constexpr int N = F::N, NR = F::NR, U0 = F::U0, W0 = F::W0, LO0 = F::LO0, E0 = 1 << W0;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t full;
+    float2* tw = reinterpret_cast<float2*>(smem_raw);
+    float2* slots = reinterpret_cast<float2*>(smem_raw + F::TW_BYTES);
+    const int tid = threadIdx.x;
+    const long long row0 = static_cast<long long>(blockIdx.x) * NR;
+    const int rows = static_cast<int>(min(static_cast<long long>(NR), n_rows - row0));
+    if (tid == 0) {
+        mbar_init(&full, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    constexpr uint32_t ROW_BYTES = static_cast<uint32_t>(sizeof(float2) * N);
+    if (tid == 0) {
+        mbar_arrive_expect_tx(&full, ROW_BYTES * static_cast<uint32_t>(rows));
+        for (int r = 0; r < rows; ++r)
+            bulk_g2s(slots + r * F::STRIDE, in + (row0 + r) * N, ROW_BYTES, &full);
+    }
+    for (int i = tid; i < N - 1; i += NT)
+        tw[i] = __ldg(tw_g + i);
+    __syncthreads();
+    mbar_wait(&full, 0);
+    // pass 1 from the natural-order rows, written back in place (swizzled)
+    float2 v[UPT][E0];
+#pragma unroll
+    for (int q = 0; q < UPT; ++q) {
+        const int u = tid + q * NT;
+        const int r = u / U0;
+        const unsigned fixed = static_cast<unsigned>(u % U0);
+        if (r < rows) {
+            const float2* slot = slots + r * F::STRIDE;
+#pragma unroll
+            for (int k = 0; k < E0; ++k)
+                v[q][k] = slot[fixed + (static_cast<unsigned>(k) << LO0)];
+            fft_stages<L, LO0, W0, true>(v[q], fixed, tw);
+        }
+    }
+    __syncthreads(); // every natural-order read of the tile is done
+#pragma unroll
+    for (int q = 0; q < UPT; ++q) {
+        const int u = tid + q * NT;
+        const int r = u / U0;
+        const unsigned fixed = static_cast<unsigned>(u % U0);
+        if (r < rows) {
+            float2* dst = slots + r * F::STRIDE + sw(fixed);
+#pragma unroll
+            for (int k = 0; k < E0; ++k)
+                dst[sw(static_cast<unsigned>(k) << LO0)] = v[q][k];
+        }
+    }
+    __syncthreads();
+    FftPasses<L, L, W, false, true, NT, 1>::run(nullptr, out, slots, F::STRIDE, rows,
+                                                LinearRows{row0, n_rows}, tw, tid, SyncCta{});
+}
+
 template <int L, int W, bool TW_SMEM, int NT>
 constexpr size_t fft_rows_smem_bytes() {
     constexpr int N = 1 << L;

@@ -554,6 +554,8 @@ int launch_fused_entry(ppfg_plan p, const FusedEntry* e, const float* taps, uint
     return check_launch("fused fir+fft kernel");
 }
 
+constexpr bool kFftTiles = true;
+
 int launch_channelize(ppfg_plan p, const float2* din, uint64_t rows, float2* dout,
                       bool fft_fallback, cudaStream_t st) {
     if (rows == 0)
@@ -599,6 +601,19 @@ int launch_channelize(ppfg_plan p, const float2* din, uint64_t rows, float2* dou
         void* args[] = {&din, &dout, &rows_ll, &p->d_tw};
         PPFG_CUDA(cudaLaunchKernel(fr.fn, dim3(static_cast<unsigned>(grid)), dim3(fr.nt), args, fr.smem, st));
         return check_launch("fft kernel (TMA ring)");
+    }
+    // K2n (C = 64..2048): non-persistent tiles of rows (in place is safe: a
+    // CTA reads all its rows before it writes any, and no other CTA touches
+    // them); TMA needs a 16-byte-aligned source
+    if (kFftTiles && L >= 6 && L <= 11 && reinterpret_cast<uintptr_t>(din) % 16 == 0) {
+        const FftEntry e = fft_tiles_entry(L);
+        PPFG_TRY(ensure_smem_attr(e.fn, e.smem, p->device));
+        const uint64_t grid = cdiv(rows, static_cast<uint64_t>(e.rows_per_tile));
+        long long rows_ll = static_cast<long long>(rows);
+        void* args[] = {&din, &dout, &rows_ll, &p->d_tw};
+        PPFG_CUDA(cudaLaunchKernel(e.fn, dim3(static_cast<unsigned>(grid)), dim3(e.nt), args, e.smem,
+                                   st));
+        return check_launch("fft kernel (tiles)");
     }
     // T = 1 fused kernel with unit taps (in place is safe: row s is written
     // only after it was read, and nothing else reads it); TMA needs a

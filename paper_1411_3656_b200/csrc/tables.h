@@ -37,6 +37,9 @@ struct FftEntry {
     int rows_per_tile;
 };
 
+// K2n tile FFT (fft.cuh fft_tiles_kernel) for 6 <= L <= 11, or {} if none
+FftEntry fft_tiles_entry(int L);
+
 constexpr int kFftW = 5;
 constexpr int kFftNT = 256;
 constexpr int kFftMaxL = 13;
