@@ -37,6 +37,19 @@ PPFG_DEV float4 tw_load(const float2* p) {
     else
         return tw_expand(__ldg(p));
 }
+// float2 twiddles in shared memory read with a volatile load: kept in program
+// order, so the compiler does not hoist a whole pass's twiddles into registers
+// (K2n's 5-bit passes would otherwise need ~200 registers)
+struct TwV2 {
+    float x, y;
+};
+template <bool TW_SMEM>
+PPFG_DEV float4 tw_load(const TwV2* p) {
+    static_assert(TW_SMEM, "shared-memory twiddles only");
+    float2 w;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(w.x), "=f"(w.y) : "r"(smem_u32(p)));
+    return tw_expand(w);
+}
 template <bool TW_SMEM>
 PPFG_DEV float4 tw_load(const float4* p) {
     if constexpr (TW_SMEM)
@@ -385,11 +398,12 @@ struct FftTiles {
     static_assert(S::NP >= 2, "pass 1 hands over to FftPasses<.., I = 1>");
 };
 
-template <int L, int W, int NT, int MINB = 1, int UPT = 1>
+template <int L, int W, int NT, int MINB = 1, int UPT = 1, bool VOLTW = false>
 __global__ void __launch_bounds__(NT, MINB) fft_tiles_kernel(const float2* __restrict__ in,
                                                        float2* __restrict__ out, long long n_rows,
                                                        const float2* __restrict__ tw_g) {
     using F = FftTiles<L, W, NT, UPT>;
+    using TWT = typename std::conditional<VOLTW, TwV2, float2>::type;
     constexpr int N = F::N, NR = F::NR, U0 = F::U0, W0 = F::W0, LO0 = F::LO0, E0 = 1 << W0;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t full;
@@ -425,7 +439,7 @@ __global__ void __launch_bounds__(NT, MINB) fft_tiles_kernel(const float2* __res
 #pragma unroll
             for (int k = 0; k < E0; ++k)
                 v[q][k] = slot[fixed + (static_cast<unsigned>(k) << LO0)];
-            fft_stages<L, LO0, W0, true>(v[q], fixed, tw);
+            fft_stages<L, LO0, W0, true>(v[q], fixed, reinterpret_cast<const TWT*>(tw));
         }
     }
     __syncthreads(); // every natural-order read of the tile is done
@@ -443,7 +457,8 @@ __global__ void __launch_bounds__(NT, MINB) fft_tiles_kernel(const float2* __res
     }
     __syncthreads();
     FftPasses<L, L, W, false, true, NT, 1>::run(nullptr, out, slots, F::STRIDE, rows,
-                                                LinearRows{row0, n_rows}, tw, tid, SyncCta{});
+                                                LinearRows{row0, n_rows},
+                                                reinterpret_cast<const TWT*>(tw), tid, SyncCta{});
 }
 
 template <int L, int W, bool TW_SMEM, int NT>
