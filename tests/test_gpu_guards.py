@@ -86,3 +86,27 @@ def test_detection_partials_stay_inside(cuda, port, C, T, mode, S):
         torch.cuda.synchronize()
     assert a.shape == (C,) and torch.equal(a, b)   # deterministic, repeatable
     assert bool(torch.isfinite(a).all())
+
+
+@pytest.mark.parametrize("C,S", [(64, 1000), (256, 333), (1024, 77), (2048, 5), (4096, 9), (8192, 3)])
+def test_channelize_writes_only_its_rows(cuda, port, C, S):
+    """channelize_block kernels (K2n row tiles with ragged last tiles, K3 at
+    T = 1, K2r): the output view sits between canary rows, the input view
+    between NaN rows; in place as well."""
+    import torch
+    ppf = _ppf()
+    x_host = ppf.synth(C, S * C, seed=C + S).reshape(S, C)
+    want = port.channelize(x_host, C).view(np.complex64).reshape(S, C)
+    xin = torch.full((S + 2 * GUARD, C), float("nan"), dtype=torch.complex64, device=cuda)
+    xin[GUARD:GUARD + S] = torch.from_numpy(x_host).to(cuda)
+    buf = torch.empty((S + 2 * GUARD, C), dtype=torch.complex64, device=cuda)
+    torch.view_as_real(buf).view(torch.int32).fill_(CANARY)
+    with ppf.Plan(C, 1, port.generate_prototype(C, 1, 9.0)) as p:
+        p.channelize(xin[GUARD:GUARD + S], out=buf[GUARD:GUARD + S])
+        p.channelize(xin[GUARD:GUARD + S], out=xin[GUARD:GUARD + S])   # in place
+        torch.cuda.synchronize()
+    raw = torch.view_as_real(buf).view(torch.int32)
+    assert bool((raw[:GUARD] == CANARY).all()) and bool((raw[GUARD + S:] == CANARY).all())
+    assert bool(torch.isnan(xin[:GUARD]).all()) and bool(torch.isnan(xin[GUARD + S:]).all())
+    assert np.array_equal(bits(buf[GUARD:GUARD + S].cpu().numpy()), bits(want))
+    assert np.array_equal(bits(xin[GUARD:GUARD + S].cpu().numpy()), bits(want))
