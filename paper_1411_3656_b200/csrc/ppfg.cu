@@ -1369,6 +1369,11 @@ int ppfg_plan_create(ppfg_plan* plan, uint64_t n_channels, uint64_t n_taps,
             }
         }
     }
+    // the table uploads above are plain cudaMemcpy calls from pageable memory,
+    // which may return before their DMA has landed; the plan's kernels run on
+    // non-blocking streams, so wait for the legacy stream once here
+    if (cudaStreamSynchronize(cudaStreamLegacy) != cudaSuccess)
+        return cleanup(fail(PPFG_CUDA_ERROR, "ppfg_plan_create: table upload failed"));
     if (cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&p->s_d2h, cudaStreamNonBlocking) != cudaSuccess)
@@ -1579,22 +1584,28 @@ static int one_row(const void* in, uint64_t n, void* out, bool fallback, const c
     if (fallback && is_pow2(n) && n > 1) { // force the naive path for dft_naive
         DeviceGuard dg(p->device);
         void* d = nullptr;
-        rc = cudaMalloc(&d, 2 * n * sizeof(float2)) == cudaSuccess ? PPFG_OK : PPFG_CUDA_ERROR;
+        double2* dr = nullptr;
+        rc = cudaMalloc(&d, 2 * n * sizeof(float2)) == cudaSuccess &&
+                     cudaMalloc(&dr, n * sizeof(double2)) == cudaSuccess
+                 ? PPFG_OK
+                 : fail(PPFG_CUDA_ERROR, "dft_naive: device allocation failed");
         if (rc == PPFG_OK) {
             const auto r = host_roots(n);
-            double2* dr = nullptr;
-            cudaMalloc(&dr, n * sizeof(double2));
-            cudaMemcpy(dr, r.data(), n * sizeof(double2), cudaMemcpyHostToDevice);
-            cudaMemcpy(d, in, n * sizeof(float2), cudaMemcpyHostToDevice);
+            // copies on the plan's (non-blocking) stream, so the kernel is
+            // ordered after them (a plain cudaMemcpy from pageable memory may
+            // return before its DMA has landed)
+            cudaMemcpyAsync(dr, r.data(), n * sizeof(double2), cudaMemcpyHostToDevice, p->stream);
+            cudaMemcpyAsync(d, in, n * sizeof(float2), cudaMemcpyHostToDevice, p->stream);
             float2* din = static_cast<float2*>(d);
             dft_naive_kernel<<<static_cast<unsigned>(cdiv(n, 256)), 256, 0, p->stream>>>(
                 din, din + n, static_cast<unsigned>(n), 1, dr);
             rc = check_launch("dft_naive kernel");
             cudaMemcpyAsync(out, din + n, n * sizeof(float2), cudaMemcpyDeviceToHost, p->stream);
-            cudaStreamSynchronize(p->stream);
-            cudaFree(dr);
-            cudaFree(d);
+            if (cudaStreamSynchronize(p->stream) != cudaSuccess && rc == PPFG_OK)
+                rc = fail(PPFG_CUDA_ERROR, "dft_naive: stream error");
         }
+        cudaFree(dr);
+        cudaFree(d);
     } else {
         rc = ppfg_channelize(p, in, 1, out, fallback ? 1 : 0, PPFG_MEM_HOST, nullptr);
     }
@@ -1781,6 +1792,8 @@ int ppfg_synth(uint64_t n_channels, uint64_t seed, uint64_t first_sample, uint64
             PPFG_CUDA(cudaMalloc(&dtone, tone.size() * sizeof(float2)));
             PPFG_CUDA(cudaMemcpy(dtone, tone.data(), tone.size() * sizeof(float2),
                                  cudaMemcpyHostToDevice));
+            // the caller's stream may be non-blocking: the DMA must have landed
+            PPFG_CUDA(cudaStreamSynchronize(cudaStreamLegacy));
             c.dev[key] = dtone;
         } else {
             dtone = it->second;
@@ -2407,8 +2420,12 @@ int ppfg_device_free(void* ptr) {
 }
 
 int ppfg_memcpy(void* dst, const void* src, uint64_t bytes) {
-    if (bytes)
+    if (bytes) {
         PPFG_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyDefault));
+        // complete on return (a copy from pageable memory may return before
+        // its DMA lands; the plans' kernels run on non-blocking streams)
+        PPFG_CUDA(cudaStreamSynchronize(cudaStreamLegacy));
+    }
     return PPFG_OK;
 }
 
