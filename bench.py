@@ -630,6 +630,10 @@ def main():
                "pcie_limit": pcie_probe(hx, hy, x, y)}
         # the same call with pageable host buffers (what a reference caller
         # holds): staged through pinned memory by the library's copy threads
+        # (one rank only: N ranks x 13 GB more host memory otherwise)
+        if world > 1:
+            del hx, hy
+    if e2e is not None and world == 1:
         px = hx.numpy().copy()
         py = np.empty((oc, C), np.complex64)
         del hx, hy
