@@ -115,6 +115,19 @@ PPFG_DEV void fft_prestages_trivial(float2 (&v)[4]) {
     v[3] = make_float2(__fsub_rn(a2.x, a3.y), __fadd_rn(a2.y, a3.x));
 }
 
+// FAST mode: the prestages with their trivial twiddles as additions for any
+// R <= 4 (R = 2: one stage, twiddle 1; R = 4: fft_prestages_trivial)
+template <int RLOG>
+PPFG_DEV void fft_prestages_trivial_r(float2 (&v)[1 << RLOG]) {
+    if constexpr (RLOG == 1) {
+        const float2 a = add2(v[0], v[1]), b = sub2(v[0], v[1]);
+        v[0] = a;
+        v[1] = b;
+    } else if constexpr (RLOG == 2) {
+        fft_prestages_trivial(v);
+    }
+}
+
 // ---- pass schedule: NP passes of near-equal width, widest first ------------------
 template <int L, int W>
 struct FftSchedule {

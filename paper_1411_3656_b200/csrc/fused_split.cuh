@@ -80,8 +80,11 @@ PPFG_DEV void set_max_regs() {
 
 template <int L_, int LQ_, int T_, bool EXACT_, int FIR_WG_ = 2, int W_ = 5,
           int FIR_REGS_ = 152, int FFT_REGS_ = 104, int PC_ = 0, bool TW4_ = false, bool HS_ = false,
-          bool PAIR_ = false>
+          bool PAIR_ = false, bool TRIV_ = false>
 struct SplitCfg {
+    // TRIV (FAST, R <= 4): the FIR role's prestages use their trivial
+    // twiddles as additions (fused.cuh FusedCfg::TRIV)
+    static constexpr bool TRIV = TRIV_;
     // PAIR: the FIR role filters two consecutive spectra per step with their
     // accumulation chains interleaved (each output still sums its taps in
     // ascending order, so results are unchanged): with R <= 2 channels per
@@ -158,6 +161,7 @@ struct SplitCfg {
     static_assert(!PAIR || (B % 2 == 0 && RB % 2 == 0 && PROWS % 2 == 0 && T >= 2),
                   "spectrum pairs within a chunk and a pass group");
     static_assert(Q >= 2 && Q <= 8, "portable cluster sizes");
+    static_assert(!TRIV || (!EXACT && RLOG >= 1 && RLOG <= 2), "trivial prestages: FAST, R = 2 or 4");
     static_assert(R >= 1 && R <= 8 && R * Q * NFIR == N, "every FIR thread owns whole channels");
     static constexpr int LAUNCH_REGS = (65536 / NT) & ~7;
     static_assert(FIR_REGS * NFIR + FFT_REGS * NFFT <= LAUNCH_REGS * NT, "register split");
@@ -459,8 +463,13 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
                             xw[k][T - 2] = a;
                         xw[k][T - 1] = bb;
                     }
-                    fft_prestages<Cfg::L, RLOG>(y0, twr);
-                    fft_prestages<Cfg::L, RLOG>(y1, twr);
+                    if constexpr (Cfg::TRIV) {
+                        fft_prestages_trivial_r<RLOG>(y0);
+                        fft_prestages_trivial_r<RLOG>(y1);
+                    } else {
+                        fft_prestages<Cfg::L, RLOG>(y0, twr);
+                        fft_prestages<Cfg::L, RLOG>(y1, twr);
+                    }
 #pragma unroll
                     for (int k = 0; k < R; ++k) {
                         const uint32_t off0 = 8u * (i * Cfg::STRIDE + slot_of[k]);
@@ -510,7 +519,10 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
                             y[k] = acc;
                         }
                     }
-                    fft_prestages<Cfg::L, RLOG>(y, twr);
+                    if constexpr (Cfg::TRIV)
+                        fft_prestages_trivial_r<RLOG>(y);
+                    else
+                        fft_prestages<Cfg::L, RLOG>(y, twr);
     #pragma unroll
                     for (int k = 0; k < R; ++k) {
                         const uint32_t off = 8u * (i * Cfg::STRIDE + slot_of[k]);

@@ -16,6 +16,9 @@ std::vector<FusedEntry> fused_part_split() {
     // EXACT T=8 lost 1-4 %). Four FIR warpgroups with one channel per thread
     // (the TSPLIT input view): EXACT T=8 0.645 -> 0.53-0.54, FAST T=16 (W=4)
     // 0.70 -> 0.70 / (W=5) 0.55 — the smaller FFT role (80 registers) loses.
+    // Trivial-twiddle prestages (SplitCfg TRIV, 13th argument, FAST): C=2048
+    // 0.739 -> 0.751, C=4096 0.577 -> 0.596; C=1024 T=16 (one prestage) 0.72
+    // either way.
     return {
         // thread-block clusters, FIR split by channel block and FFT by
         // spectrum (fused_split.cuh) — for FIR state that does not fit one SM.
@@ -40,9 +43,9 @@ std::vector<FusedEntry> fused_part_split() {
         split_entry<SplitCfg<10, 2, 32, false, 2, 5, 152, 104, 0, true, true>>(false),
         split_entry<SplitCfg<10, 1, 8, true, 2, 5, 136, 120, 0, true, true>>(true),
         split_entry<SplitCfg<10, 2, 16, true, 2, 5, 152, 104, 0, true, true, true>>(true),
-        split_entry<SplitCfg<11, 1, 8, false, 2, 5, 136, 120, 0, false, true>>(true),
+        split_entry<SplitCfg<11, 1, 8, false, 2, 5, 136, 120, 0, false, true, false, true>>(true),
         split_entry<SplitCfg<11, 2, 8, true, 2, 5, 152, 104, 0, true, false, true>>(true),
-        split_entry<SplitCfg<12, 2, 8, false, 2, 5, 168, 88, 0, false, true>>(true),
+        split_entry<SplitCfg<12, 2, 8, false, 2, 5, 168, 88, 0, false, true, false, true>>(true),
         split_entry<SplitCfg<13, 3, 8, false>>(false),
     };
 }
