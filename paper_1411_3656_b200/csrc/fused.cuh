@@ -126,7 +126,7 @@ struct FusedCfg {
     static_assert(BU * B <= 32, "FIR unroll too large");
     static_assert(!HS || FFT_SPLIT, "per-pass-group handoff needs an evenly split tile");
     static_assert(!HS || 1 + 2 * NTILE * PGROUPS + PGROUPS <= 16, "named barriers");
-    static_assert(!TRIV || (!EXACT && RLOG == 2), "trivial prestages: FAST, R = 4");
+    static_assert(!TRIV || (!EXACT && RLOG >= 1 && RLOG <= 2), "trivial prestages: FAST, R = 2 or 4");
     static_assert(!PAIR || (B % 2 == 0 && T >= 2 && (!HS || PROWS % 2 == 0)),
                   "spectrum pairs within a batch and a pass group");
     // named barrier ids (0 = __syncthreads): FULL[t][pg], EMPTY[t][pg], pass
@@ -422,8 +422,8 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
                         xw[k][T - 1] = bb;
                     }
                     if constexpr (Cfg::TRIV) {
-                        fft_prestages_trivial(y0);
-                        fft_prestages_trivial(y1);
+                        fft_prestages_trivial_r<RLOG>(y0);
+                        fft_prestages_trivial_r<RLOG>(y1);
                     } else {
                         fft_prestages<L, RLOG>(y0, twr);
                         fft_prestages<L, RLOG>(y1, twr);
@@ -474,7 +474,7 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
                         }
                     }
                     if constexpr (Cfg::TRIV)
-                        fft_prestages_trivial(y);
+                        fft_prestages_trivial_r<RLOG>(y);
                     else
                         fft_prestages<L, RLOG>(y, twr);
     #pragma unroll

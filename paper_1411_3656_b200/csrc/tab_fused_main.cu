@@ -33,6 +33,9 @@ std::vector<FusedEntry> fused_part_main() {
     // T=4 kept: 0.885 vs 0.865-0.883), C=128 T=16 R=1 0.763 -> 0.908, EXACT
     // C=128 T=8 R=1 0.745 -> 0.785, EXACT C=256 T=4 R=2 0.745 -> 0.905 (one
     // step fewer lost at C=64 T=4/8, C=128 T=4, EXACT C=256 T=8, C=512 T=4).
+    // Late round 2: the one-stage trivial prestage (TRIV at R = 2) where it
+    // measured faster: C=128 T=8 0.969 -> 0.975, C=512 T=16 0.857 -> 0.864
+    // (cfg1 C=512 T=8 lost 0.6 %, C=64 even).
     // Late round 2: C=1024 T=4 FAST on three FFT warpgroups with float4
     // twiddles (the SKA entry's split) 0.888 -> 0.92-0.93; the same split
     // lost for EXACT C=512 T=8 (0.80 -> 0.71) and detection (0.448 -> 0.427).
@@ -55,10 +58,10 @@ std::vector<FusedEntry> fused_part_main() {
         power_entry<FusedCfg<10, 8, 2, false, 160, 96, 2, 2, 2, true, 0, true, true>>(),
         fused_entry<FusedCfg<9, 8, 1, false, 120, 80, 2, 3, 2, false, 0, true>>(),
         fused_entry<FusedCfg<8, 8, 0, false, 120, 80, 2, 3, 2, false, 0, true>>(),
-        fused_entry<FusedCfg<7, 8, 1, false, 120, 80, 2, 3, 2, false, 0, true>>(),
+        fused_entry<FusedCfg<7, 8, 1, false, 120, 80, 2, 3, 2, false, 0, true, true>>(),
         fused_entry<FusedCfg<6, 8, 1, false, 120, 80, 2, 3, 2, true, 0, true>>(),
         fused_entry<FusedCfg<10, 4, 2, false, 120, 80, 2, 3, 2, true, 0, true, true>>(),
-        fused_entry<FusedCfg<9, 16, 1, false, 136, 120, 4, 2, 2, false, 0, true>>(),
+        fused_entry<FusedCfg<9, 16, 1, false, 136, 120, 4, 2, 2, false, 0, true, true>>(),
         fused_entry<FusedCfg<9, 8, 1, true, 160, 96, 4, 2, 2, true, 0, true>>(),
         fused_entry<FusedCfg<8, 8, 1, true, 160, 96, 4, 2, 2, true, 0, true>>(),
         fused_entry<FusedCfg<7, 8, 0, true, 160, 96, 4, 2, 2, true, 0, true, false, true>>(),
