@@ -562,10 +562,9 @@ def test_misaligned_device_views(cuda, port, C, T, flags):
     assert _rel(mp.cpu().numpy(), port.mean_power(port.fir_fft(x, C, T, coeffs), C)) <= 2e-5 * np.log2(C)
 
 
-# EXACT mode converts samples to double and results to float on the integer
-# pipe (common.cuh f2d_alu / d2f_alu) with a hardware fallback for the values
-# that path does not cover: zeros of both signs, float subnormals in and out,
-# magnitudes at the ends of the float range, and all-zero stretches (zero
+# EXACT mode on the values where float <-> double conversion and the FFT's
+# FP32 arithmetic are easiest to get wrong: zeros of both signs, float
+# subnormals in and out, large magnitudes, and all-zero stretches (zero
 # outputs) must come out bit-identical to the reference.
 @pytest.mark.parametrize("C,T", [(1024, 8), (512, 8), (64, 8), (1024, 16), (256, 4), (2048, 8),
                                  (8, 8), (1024, 32)])
