@@ -227,8 +227,12 @@ PPFG_DEV void fft_tile_pass(const float2* gin, float2* gout,
 // label) instead of storing bins to global — used when more stages follow
 // (the cluster kernel's cross-CTA stages).
 // POWER: the last pass accumulates bin powers into pacc (see fft_tile_pass).
+// LAST_GLOBAL: the last pass reads its twiddles from global memory (tw_last,
+// the full table; its lanes read consecutive entries) while the earlier
+// passes read `tw` — so a kernel needs only the first 2^(L - w_last) - 1
+// entries in shared memory (K2n at C = 4096, 8192)
 template <int L, int LREM, int W, bool FIRST_GLOBAL, bool TW_SMEM, int NT, int I = 0,
-          bool STORE_LAST = true, bool POWER = false>
+          bool STORE_LAST = true, bool POWER = false, bool LAST_GLOBAL = false>
 struct FftPasses {
     using S = FftSchedule<LREM, W>;
     static constexpr int WI = S::width(I);
@@ -238,13 +242,18 @@ struct FftPasses {
     template <class RowMap, class Sync, class TW, class PA = double>
     PPFG_DEV static void run(const float2* gin, float2* gout, float2* tile, unsigned row_stride,
                              int rows, const RowMap& map, const TW* tw, int tid,
-                             const Sync& sync, PA* pacc = nullptr) {
-        fft_tile_pass<L, LO, WI, FIRST_GLOBAL && I == 0, LAST && STORE_LAST, TW_SMEM, NT,
-                      LAST && POWER>(gin, gout, tile, row_stride, rows, map, tw, tid, pacc);
+                             const Sync& sync, PA* pacc = nullptr,
+                             const float2* __restrict__ tw_last = nullptr) {
+        if constexpr (LAST && LAST_GLOBAL)
+            fft_tile_pass<L, LO, WI, FIRST_GLOBAL && I == 0, STORE_LAST, false, NT, POWER>(
+                gin, gout, tile, row_stride, rows, map, tw_last, tid, pacc);
+        else
+            fft_tile_pass<L, LO, WI, FIRST_GLOBAL && I == 0, LAST && STORE_LAST, TW_SMEM, NT,
+                          LAST && POWER>(gin, gout, tile, row_stride, rows, map, tw, tid, pacc);
         if constexpr (!LAST) {
             sync();
-            FftPasses<L, LREM, W, FIRST_GLOBAL, TW_SMEM, NT, I + 1, STORE_LAST, POWER>::run(
-                gin, gout, tile, row_stride, rows, map, tw, tid, sync, pacc);
+            FftPasses<L, LREM, W, FIRST_GLOBAL, TW_SMEM, NT, I + 1, STORE_LAST, POWER, LAST_GLOBAL>::run(
+                gin, gout, tile, row_stride, rows, map, tw, tid, sync, pacc, tw_last);
         }
     }
 };
@@ -287,104 +296,7 @@ __global__ void __launch_bounds__(NT) fft_rows_kernel(const float2* in, float2* 
     }
 }
 
-// K2r: channelize_block (dft.hpp:175-235; FftPlan::transform, dft.hpp:100-148)
-// for large power-of-two C (one row = 2^L c64 does not
-// leave room for K3's FIR/FFT tiles), one CTA per SM, rows strided over the
-// grid. Two row slots in shared memory, each loaded by ONE TMA bulk copy
-// (cp.async.bulk, SASS UBLKCP) of the natural-order row: while one slot's
-// row is transformed, the next row lands in the other, so HBM reads overlap
-// all three passes (K2 instead waits on its first pass's global loads).
-// Pass 1 reads the natural-order row (lanes = consecutive channels,
-// conflict-free) into registers — the whole row, one unit per thread — and,
-// after a barrier, writes it back IN PLACE at swizzled slots (the slot is
-// sized for the swizzled row); later passes are in place (each unit rewrites
-// its own elements) and the last stores bins to HBM. Twiddles (float2,
-// N - 1 entries) stay in shared memory. Same butterflies as K2: bit-exact.
-// K2r: also prefetch the next row to be copied into L2 (measured +0.5-1 %)
-constexpr bool kRingL2Ahead = true;
-
-template <int L, int W, int NT_ = 0>
-struct FftRing {
-    using S = FftSchedule<L, W>;
-    static constexpr int N = 1 << L;
-    static constexpr int W0 = S::width(0), LO0 = S::lo(0);
-    static constexpr int U0 = N >> W0;                // first-pass units: the whole row
-    static constexpr int NT = NT_ > 0 ? NT_ : U0;     // (threads >= U0 idle in pass 1)
-    static_assert(NT >= U0, "pass 1 holds the whole row in registers");
-    static constexpr unsigned STRIDE = sw_row_stride(N);
-    static constexpr size_t TW_BYTES = sizeof(float2) * N;
-    static constexpr size_t SLOT_BYTES = (sizeof(float2) * STRIDE + 127) & ~size_t(127);
-    static constexpr size_t SMEM = TW_BYTES + 2 * SLOT_BYTES + 2 * sizeof(uint64_t);
-    static_assert(S::NP >= 2, "pass 1 hands over to FftPasses<.., I = 1>");
-};
-
-template <int L, int W, int NT_ = 0>
-__global__ void __launch_bounds__(FftRing<L, W, NT_>::NT, 1)
-    fft_ring_kernel(const float2* __restrict__ in, float2* __restrict__ out, long long n_rows,
-                    const float2* __restrict__ tw_g) {
-    using F = FftRing<L, W, NT_>;
-    constexpr int N = F::N, NT = F::NT, W0 = F::W0, LO0 = F::LO0, E0 = 1 << W0;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    float2* tw = reinterpret_cast<float2*>(smem_raw);
-    float2* slots = reinterpret_cast<float2*>(smem_raw + F::TW_BYTES);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + F::TW_BYTES + 2 * F::SLOT_BYTES);
-    const int tid = threadIdx.x;
-    for (int i = tid; i < N - 1; i += NT)
-        tw[i] = tw_g[i];
-    if (tid == 0) {
-        mbar_init(full, 1);
-        mbar_init(full + 1, 1);
-        fence_mbar_init();
-    }
-    __syncthreads();
-    const long long step = gridDim.x;
-    constexpr uint32_t ROW_BYTES = static_cast<uint32_t>(sizeof(float2) * N);
-    auto issue = [&](long long row, int s) {
-        mbar_arrive_expect_tx(full + s, ROW_BYTES);
-        bulk_g2s(reinterpret_cast<unsigned char*>(slots) + s * F::SLOT_BYTES, in + row * N, ROW_BYTES,
-                 full + s);
-    };
-    if (tid == 0) {
-        if (blockIdx.x < n_rows)
-            issue(blockIdx.x, 0);
-        if (blockIdx.x + step < n_rows)
-            issue(blockIdx.x + step, 1);
-    }
-    int i = 0;
-    for (long long row = blockIdx.x; row < n_rows; row += step, ++i) {
-        const int s = i & 1;
-        float2* slot = reinterpret_cast<float2*>(reinterpret_cast<unsigned char*>(slots) + s * F::SLOT_BYTES);
-        mbar_wait(full + s, static_cast<uint32_t>((i >> 1) & 1));
-        const bool p1 = tid < F::U0;
-        const unsigned fixed = static_cast<unsigned>(p1 ? tid : 0);
-        float2 v[E0];
-        if (p1) {
-#pragma unroll
-            for (int k = 0; k < E0; ++k)
-                v[k] = slot[fixed + (static_cast<unsigned>(k) << LO0)];
-            fft_stages<L, LO0, W0, true>(v, fixed, tw);
-        }
-        __syncthreads(); // every natural-order read of the slot is done
-        if (p1) {
-            float2* dst = slot + sw(fixed);
-#pragma unroll
-            for (int k = 0; k < E0; ++k)
-                dst[sw(static_cast<unsigned>(k) << LO0)] = v[k];
-        }
-        __syncthreads();
-        FftPasses<L, L, W, false, true, NT, 1>::run(nullptr, out, slot, F::STRIDE, 1,
-                                                    LinearRows{row, n_rows}, tw, tid, SyncCta{});
-        __syncthreads(); // every read of the slot is done: refill it
-        if (tid == 0 && row + 2 * step < n_rows) {
-            fence_proxy_async();
-            issue(row + 2 * step, s);
-            if (kRingL2Ahead && row + 3 * step < n_rows) // warm L2 for the row after it
-                bulk_prefetch_l2(in + (row + 3 * step) * N, ROW_BYTES);
-        }
-    }
-}
-
-// K2n: channelize_block for 64 <= C <= 4096 as a NON-persistent grid of small
+// K2n: channelize_block for 64 <= C <= 8192 as a NON-persistent grid of small
 // CTAs, one tile of NR rows each (NR * C * 8 B = 16-64 KB), several CTAs per
 // SM, dispatched in row order. Each CTA loads its rows with one TMA bulk copy
 // per row into a swizzled-row slot, runs the first pass from the natural-order
@@ -393,11 +305,11 @@ __global__ void __launch_bounds__(FftRing<L, W, NT_>::NT, 1)
 // Twiddles: each CTA copies the table into shared memory while its rows land
 // (read straight from global the compiler hoists a pass's twiddle loads and
 // spills). Same
-// butterflies as K2 / K2r / K3: bit-exact. The grid sweeps HBM as one narrow
+// butterflies as K2 / K3: bit-exact. The grid sweeps HBM as one narrow
 // front, the access pattern that streamed fastest of everything measured here
 // (profiles/round2/probes: a non-persistent block copy 6.78 TB/s vs 6.0-6.4
 // persistent).
-template <int L, int W, int NT, int UPT = 1>
+template <int L, int W, int NT, int UPT = 1, bool TWL = false>
 struct FftTiles {
     using S = FftSchedule<L, W>;
     static constexpr int N = 1 << L;
@@ -405,17 +317,19 @@ struct FftTiles {
     static constexpr int U0 = N >> W0;               // first-pass units per row
     static constexpr int NR = UPT * NT / U0;         // rows per CTA: UPT units per thread
     static constexpr unsigned STRIDE = sw_row_stride(N);
-    static constexpr size_t TW_BYTES = (sizeof(float2) * N + 127) & ~size_t(127);
+    // TWL: only the entries of the passes before the last in shared memory
+    static constexpr int TW_N = TWL ? (1 << (L - S::width(S::NP - 1))) - 1 : N - 1;
+    static constexpr size_t TW_BYTES = (sizeof(float2) * (TW_N + 1) + 127) & ~size_t(127);
     static constexpr size_t SMEM = TW_BYTES + sizeof(float2) * size_t(NR) * STRIDE;
     static_assert((UPT * NT) % U0 == 0 && NR >= 1, "whole rows of first-pass units");
     static_assert(S::NP >= 2, "pass 1 hands over to FftPasses<.., I = 1>");
 };
 
-template <int L, int W, int NT, int MINB = 1, int UPT = 1, bool VOLTW = false>
+template <int L, int W, int NT, int MINB = 1, int UPT = 1, bool VOLTW = false, bool TWL = false>
 __global__ void __launch_bounds__(NT, MINB) fft_tiles_kernel(const float2* __restrict__ in,
                                                        float2* __restrict__ out, long long n_rows,
                                                        const float2* __restrict__ tw_g) {
-    using F = FftTiles<L, W, NT, UPT>;
+    using F = FftTiles<L, W, NT, UPT, TWL>;
     using TWT = typename std::conditional<VOLTW, TwV2, float2>::type;
     constexpr int N = F::N, NR = F::NR, U0 = F::U0, W0 = F::W0, LO0 = F::LO0, E0 = 1 << W0;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -436,7 +350,7 @@ __global__ void __launch_bounds__(NT, MINB) fft_tiles_kernel(const float2* __res
         for (int r = 0; r < rows; ++r)
             bulk_g2s(slots + r * F::STRIDE, in + (row0 + r) * N, ROW_BYTES, &full);
     }
-    for (int i = tid; i < N - 1; i += NT)
+    for (int i = tid; i < F::TW_N; i += NT)
         tw[i] = __ldg(tw_g + i);
     __syncthreads();
     mbar_wait(&full, 0);
@@ -469,9 +383,9 @@ __global__ void __launch_bounds__(NT, MINB) fft_tiles_kernel(const float2* __res
         }
     }
     __syncthreads();
-    FftPasses<L, L, W, false, true, NT, 1>::run(nullptr, out, slots, F::STRIDE, rows,
-                                                LinearRows{row0, n_rows},
-                                                reinterpret_cast<const TWT*>(tw), tid, SyncCta{});
+    FftPasses<L, L, W, false, true, NT, 1, true, false, TWL>::run(
+        nullptr, out, slots, F::STRIDE, rows, LinearRows{row0, n_rows},
+        reinterpret_cast<const TWT*>(tw), tid, SyncCta{}, static_cast<double*>(nullptr), tw_g);
 }
 
 template <int L, int W, bool TW_SMEM, int NT>

@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(Cfg::NT, 1)
 #if PPFG_L2X_DEBUG != 2
             // first pass: natural-order rows -> registers (one unit per
             // thread); after the group barrier, back in place at swizzled
-            // slots (as K2r, fft.cuh)
+            // slots (the first pass rewrites each natural-order row in place)
             static_assert(BT * U0 == FNT, "one first-pass unit per FFT thread");
             {
                 const int r = ftid / U0;

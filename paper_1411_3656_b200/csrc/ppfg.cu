@@ -216,8 +216,6 @@ struct ppfg_plan_s {
     float2* d_tw = nullptr;      // FftPlan twiddles (wr, wi), C-1 entries
     float4* d_tw4 = nullptr;     // the same, pre-expanded (wr, wi, -wi, wr)
     double2* d_roots = nullptr;  // dft_naive roots, C entries (non-pow2)
-    float* d_ones = nullptr;     // C unit taps: channelize through the T = 1 fused kernel
-    const FusedEntry* fft_fused = nullptr;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     const FusedEntry* fused = nullptr;
@@ -581,24 +579,10 @@ int launch_channelize(ppfg_plan p, const float2* din, uint64_t rows, float2* dou
         return rc;
     }
     const int L = p->L;
-    // C = 8192: the TMA-ring row FFT (0.73 of the HBM roofline vs 0.57 for
-    // K2; at C = 4096 it measured 0.82 vs 0.83 for the T = 1 fused kernel)
-    if (L == 13 && reinterpret_cast<uintptr_t>(din) % 16 == 0) {
-        const FftEntry fr = fft_ring_entry();
-        PPFG_TRY(ensure_smem_attr(fr.fn, fr.smem, p->device));
-        int per_sm = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fr.fn, fr.nt, fr.smem);
-        const uint64_t grid =
-            std::min<uint64_t>(rows, static_cast<uint64_t>(p->num_sms) * std::max(per_sm, 1));
-        long long rows_ll = static_cast<long long>(rows);
-        void* args[] = {&din, &dout, &rows_ll, &p->d_tw};
-        PPFG_CUDA(cudaLaunchKernel(fr.fn, dim3(static_cast<unsigned>(grid)), dim3(fr.nt), args, fr.smem, st));
-        return check_launch("fft kernel (TMA ring)");
-    }
-    // K2n (C = 64..2048): non-persistent tiles of rows (in place is safe: a
+    // K2n (C = 64..8192): non-persistent tiles of rows (in place is safe: a
     // CTA reads all its rows before it writes any, and no other CTA touches
     // them); TMA needs a 16-byte-aligned source
-    if (kFftTiles && L >= 6 && L <= 11 && reinterpret_cast<uintptr_t>(din) % 16 == 0) {
+    if (kFftTiles && L >= 6 && L <= 13 && reinterpret_cast<uintptr_t>(din) % 16 == 0) {
         const FftEntry e = fft_tiles_entry(L);
         PPFG_TRY(ensure_smem_attr(e.fn, e.smem, p->device));
         const uint64_t grid = cdiv(rows, static_cast<uint64_t>(e.rows_per_tile));
@@ -608,11 +592,6 @@ int launch_channelize(ppfg_plan p, const float2* din, uint64_t rows, float2* dou
                                    st));
         return check_launch("fft kernel (tiles)");
     }
-    // T = 1 fused kernel with unit taps (in place is safe: row s is written
-    // only after it was read, and nothing else reads it); TMA needs a
-    // 16-byte-aligned source
-    if (p->fft_fused && reinterpret_cast<uintptr_t>(din) % 16 == 0)
-        return launch_fused_entry(p, p->fft_fused, p->d_ones, 1, din, rows, dout, st);
     if (const FftEntry* e = fft_table(L)) {
         PPFG_TRY(ensure_smem_attr(e->fn, e->smem, p->device));
         const uint64_t tiles = cdiv(rows, static_cast<uint64_t>(e->rows_per_tile));
@@ -1356,19 +1335,6 @@ int ppfg_plan_create(ppfg_plan* plan, uint64_t n_channels, uint64_t n_taps,
                        cudaMemcpyHostToDevice) != cudaSuccess)
             return cleanup(fail(PPFG_CUDA_ERROR, "ppfg_plan_create: root upload failed"));
     }
-    if (p->L >= 0) {
-        for (const auto& e : fused_table()) {
-            if (!e.power_only && e.L == p->L && e.T == 1 && e.q == 1) {
-                std::vector<float> ones(n_channels, 1.0f);
-                if (cudaMalloc(&p->d_ones, n_channels * sizeof(float)) != cudaSuccess ||
-                    cudaMemcpy(p->d_ones, ones.data(), n_channels * sizeof(float),
-                               cudaMemcpyHostToDevice) != cudaSuccess)
-                    return cleanup(fail(PPFG_CUDA_ERROR, "ppfg_plan_create: unit taps failed"));
-                p->fft_fused = &e;
-                break;
-            }
-        }
-    }
     // the table uploads above are plain cudaMemcpy calls from pageable memory,
     // which may return before their DMA has landed; the plan's kernels run on
     // non-blocking streams, so wait for the legacy stream once here
@@ -1428,7 +1394,6 @@ int ppfg_plan_destroy(ppfg_plan p) {
     cudaFree(p->d_tw);
     cudaFree(p->d_tw4);
     cudaFree(p->d_roots);
-    cudaFree(p->d_ones);
     cudaFree(p->d_part);
     cudaFree(p->d_bins);
     cudaFree(p->d_ring);

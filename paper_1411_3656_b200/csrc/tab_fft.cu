@@ -1,9 +1,7 @@
-// tab_fft.cu — K2 row FFT and K2r TMA-ring FFT instantiations.
+// tab_fft.cu — K2 row FFT and K2n tile FFT instantiations.
 #include "tables_impl.cuh"
 
 namespace ppfg {
-
-constexpr int kRingNT = 0; // K2r threads per CTA (0: one first-pass unit per thread; 512 measured the same)
 
 template <int L>
 FftEntry fft_entry() {
@@ -24,19 +22,24 @@ const FftEntry* fft_table(int L) {
     return &t[L];
 }
 
-template <int L, int NT, int MINB = 1, int W = kFftW, int UPT = 1, bool VOLTW = false>
+template <int L, int NT, int MINB = 1, int W = kFftW, int UPT = 1, bool VOLTW = false,
+          bool TWL = false>
 FftEntry fft_tiles_one() {
-    using F = FftTiles<L, W, NT, UPT>;
-    return {reinterpret_cast<KernelFn>(&fft_tiles_kernel<L, W, NT, MINB, UPT, VOLTW>), F::SMEM, NT,
-            F::NR};
+    using F = FftTiles<L, W, NT, UPT, TWL>;
+    return {reinterpret_cast<KernelFn>(&fft_tiles_kernel<L, W, NT, MINB, UPT, VOLTW, TWL>), F::SMEM,
+            NT, F::NR};
 }
 
 // Per C the (threads, units per thread, pass width) that measured fastest
 // (1 GiB back to back, fraction of the measured HBM peak; the earlier
 // channelize_block kernel K3(T=1) in brackets; cuFFT after the slash):
 // C=64 1.03 (0.88) / 0.99, C=128 1.04 (0.94) / 1.04, C=256 1.04 (0.94) / 1.05,
-// C=512 1.04 (0.95) / 1.04, C=1024 1.01 (0.92) / 1.04, C=2048 0.91 (0.88) / 0.97.
-// At C=4096 the K3(T=1) kernel stays (0.86 vs 0.81-0.86). C=1024 needs the
+// C=512 1.04 (0.95) / 1.04, C=1024 1.01 (0.92) / 1.04, C=2048 0.97 (0.88) / 0.97,
+// C=4096 0.95 (0.86) / 0.92, C=8192 0.84 (K2r, a persistent TMA-ring kernel
+// with the whole 64 KB table in shared memory: 0.76) / 0.80. From C=2048 the
+// tiles keep only the first passes' twiddles in shared memory (TWL: 2-4 KB
+// instead of 16-64 KB) and the last pass reads them from global (its lanes
+// read consecutive entries). C=1024 needs the
 // volatile twiddle loads (TwV2): with ordinary loads its 5-bit passes take
 // 198 registers (0.80), 4-bit passes 0.935. Rejected per C: 512-thread tiles
 // (0.54-0.60), 16 KB tiles at C=64/256 (0.80-0.81), 6-bit passes at C=2048
@@ -48,15 +51,13 @@ FftEntry fft_tiles_entry(int L) {
     case 8: return fft_tiles_one<8, 128, 1, kFftW, 2>();   // 16 rows
     case 9: return fft_tiles_one<9, 128>();                // 8 rows
     case 10: return fft_tiles_one<10, 128, 1, kFftW, 1, true>(); // 4 rows, volatile twiddle loads
-    case 11: return fft_tiles_one<11, 256, 1, kFftW, 2>(); // 4 rows (64 KB)
-    case 12: return {}; // K3(T=1)
+    // C >= 2048: only the first passes' twiddles in shared memory, the last
+    // pass reads the table from global (TWL)
+    case 11: return fft_tiles_one<11, 128, 1, kFftW, 2, false, true>(); // 2 rows
+    case 12: return fft_tiles_one<12, 128, 1, kFftW, 2, false, true>(); // 1 row
+    case 13: return fft_tiles_one<13, 128, 1, kFftW, 2, false, true>(); // 1 row (64 KB)
     default: return {};
     }
-}
-
-FftEntry fft_ring_entry() {
-    using F = FftRing<13, kFftW, kRingNT>;
-    return {reinterpret_cast<KernelFn>(&fft_ring_kernel<13, kFftW, kRingNT>), F::SMEM, F::NT, 1};
 }
 
 } // namespace ppfg

@@ -1,12 +1,13 @@
-// tab_fused_fft.cu — K3 with T = 1 and unit taps: the bit-exact TMA-fed FFT used by channelize_block.
+// tab_fused_fft.cu — K3 with T = 1: fir+fft plans with a single tap (channelize_block itself
+// takes the K2n tile FFT since late round 2).
 #include "tables_impl.cuh"
 
 namespace ppfg {
 
 std::vector<FusedEntry> fused_part_fft() {
     return {
-        // T = 1 with unit taps: x*1 == x exactly, so these are bit-exact,
-        // TMA-fed, warp-specialised FFTs — channelize_block for 64 <= C <= 4096
+        // T = 1: x*h with one tap, then the bit-exact FFT; until late round 2
+        // also channelize_block (unit taps) for 64 <= C <= 4096
         // (C = 4096: 0.76 of roofline vs 0.69 for K2)
         // (split-kernel T = 1 entries for C = 4096, 8192 and FP64 C = 4096 on
         // 8-CTA clusters measured slower than K2 / the unfused path)

@@ -37,7 +37,7 @@ struct FftEntry {
     int rows_per_tile;
 };
 
-// K2n tile FFT (fft.cuh fft_tiles_kernel) for 6 <= L <= 11, or {} if none
+// K2n tile FFT (fft.cuh fft_tiles_kernel) for 6 <= L <= 13, or {} if none
 FftEntry fft_tiles_entry(int L);
 
 constexpr int kFftW = 5;
@@ -73,7 +73,6 @@ std::vector<FusedEntry> fused_part_fft();    // tab_fused_fft.cu
 std::vector<FusedEntry> fused_part_split();  // tab_split.cu
 
 const FftEntry* fft_table(int L);   // K2, tab_fft.cu
-FftEntry fft_ring_entry();          // K2r at C = 8192, tab_fft.cu
 FirTmaEntry fir_tma_table(int T);   // K1t, tab_fir.cu
 FirTmaEntry fir_fast_table(int T);  // K1f, tab_fir.cu
 FirBlkEntry fir_blk_table(int T, bool exact); // K1b, tab_fir_blk.cu

@@ -1,6 +1,6 @@
 """One small launch of every kernel family, for compute-sanitizer
 (racecheck / synccheck / memcheck): K3 fused FP32 and FP64, K3s cluster
-kernels (FP32 T=16, FP64 T=8, C=4096), K1b FIR (T=64), K2r (C=8192), the T=1
+kernels (FP32 T=16, FP64 T=8, C=4096), K1b FIR (T=64), K2n (C=8192), the T=1
 fused FFT, K4 dft_naive, detection. Each result is also checked against the
 oracle so a run under the sanitizer is a correctness run too.
 
@@ -26,7 +26,7 @@ CASES = [  # (C, T, flags, S_in)
     (4096, 8, ppf.FAST, 24),                      # K3s C = 4096
     (1024, 64, ppf.FAST, 200),                    # K1b FP32 + T=1 fused FFT
     (256, 64, ppf.EXACT, 150),                    # K1b FP64 + K3 T=1
-    (8192, 8, ppf.FAST, 12),                      # K1t + K2r
+    (8192, 8, ppf.FAST, 12),                      # K1t + K2n
     (100, 4, ppf.EXACT, 40),                      # K1 + K4 dft_naive
 ]
 for C, T, flags, S in CASES:

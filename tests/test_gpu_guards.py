@@ -34,7 +34,7 @@ CASES = [
     (32, 32, "fast", 2000, "K6 T = 32"),
     (1024, 32, "fast", 900, "unfused K1b + K3(T=1)"),
     (1024, 64, "exact", 500, "unfused K1b FP64"),
-    (8192, 8, "fast", 40, "K1t + K2r"),
+    (8192, 8, "fast", 40, "K1t + K2n"),
     (100, 4, "exact", 90, "K1 + K4 dft_naive"),
     (1024, 32, "fast+l2x", 1300, "K7 L2 exchange"),
     (8192, 8, "exact+l2x", 300, "K7 at C = 8192"),
@@ -90,9 +90,9 @@ def test_detection_partials_stay_inside(cuda, port, C, T, mode, S):
 
 @pytest.mark.parametrize("C,S", [(64, 1000), (256, 333), (1024, 77), (2048, 5), (4096, 9), (8192, 3)])
 def test_channelize_writes_only_its_rows(cuda, port, C, S):
-    """channelize_block kernels (K2n row tiles with ragged last tiles, K3 at
-    T = 1, K2r): the output view sits between canary rows, the input view
-    between NaN rows; in place as well."""
+    """channelize_block (K2n row tiles, ragged last tiles; shared or global
+    last-pass twiddles): the output view sits between canary rows, the input
+    view between NaN rows; in place as well."""
     import torch
     ppf = _ppf()
     x_host = ppf.synth(C, S * C, seed=C + S).reshape(S, C)

@@ -147,8 +147,8 @@ def test_fft_bitwise_vs_oracle(cuda, port, L):
     assert np.array_equal(bits(got), bits(port.channelize(x, n)))
 
 
-# K2r (C = 8192): many rows per CTA, so both row slots are reused with
-# alternating mbarrier phases; in place and out of place.
+# C = 8192 channelize (K2n, one 64 KB row per CTA, twiddles of the last pass
+# from global): ragged row counts, in place and out of place.
 @pytest.mark.parametrize("rows", [1, 2, 149, 700])
 def test_fft_ring_many_rows(cuda, port, rows):
     import torch
