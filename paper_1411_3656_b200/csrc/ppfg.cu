@@ -545,8 +545,6 @@ int launch_fused_entry(ppfg_plan p, const FusedEntry* e, const float* taps, uint
     return check_launch("fused fir+fft kernel");
 }
 
-constexpr bool kFftTiles = true;
-
 int launch_channelize(ppfg_plan p, const float2* din, uint64_t rows, float2* dout,
                       bool fft_fallback, cudaStream_t st) {
     if (rows == 0)
@@ -582,7 +580,7 @@ int launch_channelize(ppfg_plan p, const float2* din, uint64_t rows, float2* dou
     // K2n (C = 64..8192): non-persistent tiles of rows (in place is safe: a
     // CTA reads all its rows before it writes any, and no other CTA touches
     // them); TMA needs a 16-byte-aligned source
-    if (kFftTiles && L >= 6 && L <= 13 && reinterpret_cast<uintptr_t>(din) % 16 == 0) {
+    if (L >= 6 && L <= 13 && reinterpret_cast<uintptr_t>(din) % 16 == 0) {
         const FftEntry e = fft_tiles_entry(L);
         PPFG_TRY(ensure_smem_attr(e.fn, e.smem, p->device));
         const uint64_t grid = cdiv(rows, static_cast<uint64_t>(e.rows_per_tile));
