@@ -397,7 +397,8 @@ def config_points(dev, peak, long_bytes):
     long stream (C=1024, T=16) at `long_bytes` (64e9 = the whole stream on one
     GPU). Per point FAST and EXACT fir_fft, and at each channel count the
     bit-exact FFT alone (channelize_block) beside cuFFT (torch.fft.fft, the
-    comparison point, not bit-exact); detection (fused mean power) at
+    comparison point, not bit-exact); at each tap count the bit-exact FIR
+    alone (ppf_fir_optimized); detection (fused mean power) at
     C=1024 T=8. Median of 5 after 2 warm-ups; frac = (in + out) / t / peak
     (detection: in / t / peak, the fused pass being read-only)."""
     import torch
@@ -434,6 +435,11 @@ def config_points(dev, peak, long_bytes):
                              "what": "channelize_block, bit-exact radix-2, in place"}
             r["cufft"] = {"ms": tc * 1e3, "frac": 2 * bo / tc / 1e9 / peak,
                           "what": "torch.fft.fft (cuFFT), comparison only, not bit-exact"}
+        if name == "taps":  # the FIR alone (ppf_fir_optimized, bit-exact)
+            with ppf.Plan(C, T, coeffs) as p:
+                t = _median_time(lambda: p.fir(x, out=y))
+            r["fir_only"] = {"ms": t * 1e3, "frac": (bi + bo) / t / 1e9 / peak,
+                             "what": "ppf_fir_optimized (fir.hpp:158-212), bit-exact"}
         if name == "taps" and T == 8:
             with ppf.Plan(C, T, coeffs, flags=ppf.FAST) as p:
                 t = _median_time(lambda: p.fir_fft_mean_power(x))
