@@ -31,19 +31,19 @@ FftEntry fft_tiles_one() {
 }
 
 // Per C the (threads, units per thread, pass width) that measured fastest
-// (1 GiB back to back, fraction of the measured HBM peak; the earlier
-// channelize_block kernel K3(T=1) in brackets; cuFFT after the slash):
-// C=64 1.03 (0.88) / 0.99, C=128 1.04 (0.94) / 1.04, C=256 1.04 (0.94) / 1.05,
-// C=512 1.04 (0.95) / 1.04, C=1024 1.01 (0.92) / 1.04, C=2048 0.97 (0.88) / 0.97,
-// C=4096 0.95 (0.86) / 0.92, C=8192 0.84 (K2r, a persistent TMA-ring kernel
-// with the whole 64 KB table in shared memory: 0.76) / 0.80. From C=2048 the
-// tiles keep only the first passes' twiddles in shared memory (TWL: 2-4 KB
-// instead of 16-64 KB) and the last pass reads them from global (its lanes
-// read consecutive entries). C=1024 needs the
-// volatile twiddle loads (TwV2): with ordinary loads its 5-bit passes take
-// 198 registers (0.80), 4-bit passes 0.935. Rejected per C: 512-thread tiles
-// (0.54-0.60), 16 KB tiles at C=64/256 (0.80-0.81), 6-bit passes at C=2048
-// (0.80-0.92).
+// (1 GiB back to back, fraction of the measured HBM peak; the kernel it
+// replaced in brackets — K3 with T = 1, at C = 8192 the persistent TMA-ring
+// K2r; cuFFT after the slash):
+//   C=64 1.03 (0.88) / 0.99    C=128 1.04 (0.94) / 1.04   C=256 1.04 (0.94) / 1.05
+//   C=512 1.04 (0.95) / 1.04   C=1024 1.01 (0.92) / 1.04  C=2048 0.97 (0.88) / 0.97
+//   C=4096 0.95 (0.86) / 0.92  C=8192 0.84 (0.76) / 0.80
+// C=1024 reads its twiddles with volatile shared loads (TwV2): with ordinary
+// loads its 5-bit passes are hoisted into 198 registers (0.80); 4-bit passes
+// 0.935. From C=2048 the tiles keep only the first passes' twiddles in shared
+// memory (TWL: 2-4 KB instead of 16-64 KB) and the last pass reads the table
+// from global (its lanes read consecutive entries). Rejected per C: 512-thread
+// tiles (0.54-0.60), 16 KB tiles at C=64/256 (0.80-0.81), 6-bit passes at
+// C=2048 (0.80-0.92), twiddles of every pass from global (0.38-0.63).
 FftEntry fft_tiles_entry(int L) {
     switch (L) {
     case 6: return fft_tiles_one<6, 128, 1, kFftW, 4>();   // 64 rows (32 KB) per CTA
